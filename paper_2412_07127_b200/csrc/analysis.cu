@@ -1,0 +1,301 @@
+// Device symbolic analysis: L/U patterns, the U->L slot map, dof-block
+// detection, level sets of both triangular sweeps and their warp schedules.
+//
+// The reference performs lower_triangle (src/sparse.cpp:189-204) and
+// csr_transpose (src/sparse.cpp:137-157) on the host on every solve and has
+// no level analysis at all (its substitution is sequential,
+// src/krylov.cpp:60-112). Here the patterns are built once in HBM and the
+// dependency DAG of each sweep is levelled so that warps can run it
+// sync-free in topological order.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "core.h"
+
+namespace pclab_b200 {
+
+namespace {
+
+__global__ void lu_counts(int64_t n, const int64_t* __restrict__ rp,
+                          const int64_t* __restrict__ dpos, int64_t* __restrict__ lcnt,
+                          int64_t* __restrict__ ucnt) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    lcnt[i] = dpos[i] - rp[i] + 1;
+    ucnt[i] = rp[i + 1] - dpos[i];
+}
+
+__global__ void lu_fill(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                        const double* __restrict__ vals, const int64_t* __restrict__ dpos,
+                        const int64_t* __restrict__ lrp, int32_t* __restrict__ lcols,
+                        double* __restrict__ lvals, const int64_t* __restrict__ urp,
+                        int32_t* __restrict__ ucols) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    int64_t o = lrp[i];
+    for (int64_t k = rp[i]; k <= dpos[i]; ++k, ++o) {
+        lcols[o] = cols[k];
+        lvals[o] = vals[k];
+    }
+    o = urp[i];
+    for (int64_t k = dpos[i]; k < rp[i + 1]; ++k, ++o) ucols[o] = cols[k];
+}
+
+// u2l[t]: U entry (i, j), j >= i, is L entry (j, i) in row j.
+__global__ void u2l_fill(int64_t n, const int64_t* __restrict__ urp,
+                         const int32_t* __restrict__ ucols, const int64_t* __restrict__ lrp,
+                         const int32_t* __restrict__ lcols, int64_t* __restrict__ u2l) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) {
+        const int32_t j = ucols[t];
+        int64_t lo = lrp[j], hi = lrp[j + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (lcols[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        u2l[t] = lo;
+    }
+}
+
+// Row i of block b = i / bs is "dense-diagonal" if its last (i % bs) + 1
+// entries are exactly columns b*bs .. i.
+__global__ void block_check(int64_t n, int bs, const int64_t* __restrict__ lrp,
+                            const int32_t* __restrict__ lcols, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int t = static_cast<int>(i % bs);
+    const int64_t e = lrp[i + 1];
+    if (e - lrp[i] < t + 1) { *bad = 1; return; }
+    for (int s = 0; s <= t; ++s)
+        if (lcols[e - 1 - s] != i - s) { *bad = 1; return; }
+}
+
+// Sync-free level computation in natural order: warps grab blocks in
+// ascending (lower) or descending (upper) order, so every dependency was
+// grabbed earlier by a running warp and the spin always terminates.
+template <bool UPPER>
+__global__ void levels_kernel(int64_t nb, int bs, const int64_t* __restrict__ rp,
+                              const int32_t* __restrict__ cols, int32_t* level,
+                              unsigned long long* counter) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1ULL);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= static_cast<unsigned long long>(nb)) return;
+        const int64_t b = UPPER ? nb - 1 - static_cast<int64_t>(t) : static_cast<int64_t>(t);
+        int lv = 0;
+        for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
+            for (int64_t k = rp[i] + lane; k < rp[i + 1]; k += 32) {
+                const int64_t jb = cols[k] / bs;
+                if (UPPER ? jb > b : jb < b) {
+                    int v;
+                    do {
+                        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(level + jb) : "memory");
+                    } while (v < 0);
+                    lv = max(lv, v + 1);
+                }
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
+        if (lane == 0)
+            asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(level + b), "r"(lv) : "memory");
+    }
+}
+
+__global__ void iota32(int32_t* p, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) p[i] = static_cast<int32_t>(i);
+}
+
+__global__ void level_starts(int64_t nb, const int32_t* __restrict__ sorted_level,
+                             int64_t* __restrict__ start) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= nb) return;
+    if (p == 0 || sorted_level[p] != sorted_level[p - 1]) start[sorted_level[p]] = p;
+}
+
+__global__ void items_per_level(int32_t nl, int64_t nb, int per_item,
+                                const int64_t* __restrict__ start, int64_t* __restrict__ nit) {
+    const int64_t l = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (l >= nl) return;
+    const int64_t end = l + 1 < nl ? start[l + 1] : nb;
+    nit[l] = (end - start[l] + per_item - 1) / per_item;
+}
+
+__global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* __restrict__ start,
+                           const int64_t* __restrict__ item_start, int64_t* __restrict__ first,
+                           int32_t* __restrict__ cnt) {
+    const int64_t l = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (l >= nl) return;
+    const int64_t s = start[l], e = l + 1 < nl ? start[l + 1] : nb;
+    int64_t it = item_start[l];
+    for (int64_t p = s; p < e; p += per_item, ++it) {
+        first[it] = p;
+        cnt[it] = static_cast<int32_t>(min(static_cast<int64_t>(per_item), e - p));
+    }
+}
+
+template <class T>
+T dev_read(const T* d, cudaStream_t st) {
+    T v;
+    CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return v;
+}
+
+void scan_inplace(int64_t* p, int64_t n, cudaStream_t st) {
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, p, p, n, st);
+    DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+    cub::DeviceScan::ExclusiveSum(t.p, tmp, p, p, n, st);
+    CK(cudaStreamSynchronize(st));
+}
+
+inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+void compute_levels(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
+                    Schedule& s, cudaStream_t st) {
+    s.bs = bs;
+    s.nblocks = n / bs;
+    s.level.alloc(std::max<int64_t>(s.nblocks, 1));
+    if (s.nblocks == 0) return;
+    CK(cudaMemsetAsync(s.level.p, 0xff, sizeof(int32_t) * s.nblocks, st));
+    DevBuf<unsigned long long> ctr(1);
+    CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned long long), st));
+    const int threads = 256;
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    if (upper)
+        levels_kernel<true><<<grid, threads, 0, st>>>(s.nblocks, bs, rp, cols, s.level.p, ctr.p);
+    else
+        levels_kernel<false><<<grid, threads, 0, st>>>(s.nblocks, bs, rp, cols, s.level.p, ctr.p);
+    CK_LAUNCH();
+}
+
+static void build_schedule(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
+                           int lanes, Schedule& s, cudaStream_t st) {
+    compute_levels(rp, cols, n, bs, upper, s, st);
+    s.lanes = lanes;
+    s.per_item = 32 / lanes;
+    const int64_t nb = s.nblocks;
+    if (nb == 0) return;
+    DevBuf<int32_t> idx(nb), sorted_lv(nb);
+    s.order.alloc(nb);
+    iota32<<<grid_for(nb, 256), 256, 0, st>>>(idx.p, nb);
+    CK_LAUNCH();
+    size_t tmp = 0;
+    const int end_bit = 32;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, s.level.p, sorted_lv.p, idx.p, s.order.p,
+                                    static_cast<int>(nb), 0, end_bit, st);
+    {
+        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceRadixSort::SortPairs(t.p, tmp, s.level.p, sorted_lv.p, idx.p, s.order.p,
+                                        static_cast<int>(nb), 0, end_bit, st);
+        CK(cudaStreamSynchronize(st));
+    }
+    s.nlevels = dev_read(sorted_lv.p + nb - 1, st) + 1;
+    DevBuf<int64_t> start(s.nlevels), nit(s.nlevels + 1);
+    level_starts<<<grid_for(nb, 256), 256, 0, st>>>(nb, sorted_lv.p, start.p);
+    items_per_level<<<grid_for(s.nlevels, 256), 256, 0, st>>>(s.nlevels, nb, s.per_item, start.p,
+                                                             nit.p);
+    CK(cudaMemsetAsync(nit.p + s.nlevels, 0, sizeof(int64_t), st));
+    CK_LAUNCH();
+    // widest level (for reporting)
+    {
+        std::vector<int64_t> hs(s.nlevels);
+        CK(cudaMemcpyAsync(hs.data(), start.p, sizeof(int64_t) * s.nlevels, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        s.max_level_width = 0;
+        for (int32_t l = 0; l < s.nlevels; ++l) {
+            const int64_t e = l + 1 < s.nlevels ? hs[l + 1] : nb;
+            s.max_level_width = std::max(s.max_level_width, e - hs[l]);
+        }
+    }
+    scan_inplace(nit.p, s.nlevels + 1, st);
+    s.nitems = dev_read(nit.p + s.nlevels, st);
+    s.item_first.alloc(s.nitems);
+    s.item_cnt.alloc(s.nitems);
+    items_fill<<<grid_for(s.nlevels, 128), 128, 0, st>>>(s.nlevels, nb, s.per_item, start.p, nit.p,
+                                                        s.item_first.p, s.item_cnt.p);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(st));
+}
+
+Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
+    if (m.an) return *m.an;
+    const DevCsr& a = m.a;
+    const int64_t n = a.n;
+    if (m.missing_diag_row >= 0)
+        throw FormatError("missing diagonal at row " + std::to_string(m.missing_diag_row));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    auto an = std::make_unique<Analysis>();
+    DevCsr& L = an->lower;
+    DevCsr& U = an->upper;
+    L.n = U.n = n;
+    L.rp.alloc(n + 1);
+    U.rp.alloc(n + 1);
+    if (n > 0) {
+        lu_counts<<<grid_for(n, 256), 256, 0, st>>>(n, a.rp.p, m.diag_pos.p, L.rp.p, U.rp.p);
+        CK_LAUNCH();
+    }
+    CK(cudaMemsetAsync(L.rp.p + n, 0, sizeof(int64_t), st));
+    CK(cudaMemsetAsync(U.rp.p + n, 0, sizeof(int64_t), st));
+    scan_inplace(L.rp.p, n + 1, st);
+    scan_inplace(U.rp.p, n + 1, st);
+    L.nnz = dev_read(L.rp.p + n, st);
+    U.nnz = dev_read(U.rp.p + n, st);
+    L.cols.alloc(L.nnz);
+    L.vals.alloc(L.nnz);
+    U.cols.alloc(U.nnz);
+    an->u2l.alloc(U.nnz);
+    if (n > 0) {
+        lu_fill<<<grid_for(n, 256), 256, 0, st>>>(n, a.rp.p, a.cols.p, a.vals.p, m.diag_pos.p,
+                                                  L.rp.p, L.cols.p, L.vals.p, U.rp.p, U.cols.p);
+        CK_LAUNCH();
+        u2l_fill<<<grid_for(n, 256), 256, 0, st>>>(n, U.rp.p, U.cols.p, L.rp.p, L.cols.p,
+                                                   an->u2l.p);
+        CK_LAUNCH();
+    }
+    // dof block size: the largest bs in {3, 2} whose diagonal blocks are
+    // dense, else 1
+    an->bs = 1;
+    for (int bs : {3, 2}) {
+        if (n == 0 || n % bs) continue;
+        DevBuf<int> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        block_check<<<grid_for(n, 256), 256, 0, st>>>(n, bs, L.rp.p, L.cols.p, bad.p);
+        CK_LAUNCH();
+        if (dev_read(bad.p, st) == 0) {
+            an->bs = bs;
+            break;
+        }
+    }
+    // lanes per block from the mean off-block entry count
+    const int bs = an->bs;
+    const double off_per_block =
+        n ? (static_cast<double>(L.nnz) - static_cast<double>(n / bs) * bs * (bs + 1) / 2.0) /
+                static_cast<double>(n / bs)
+          : 0.0;
+    int lanes = 2;
+    while (lanes < 32 && lanes < off_per_block) lanes *= 2;
+    build_schedule(L.rp.p, L.cols.p, n, 1, false, 32, an->row_lo, st);
+    build_schedule(L.rp.p, L.cols.p, n, bs, false, lanes, an->blk_lo, st);
+    build_schedule(U.rp.p, U.cols.p, n, bs, true, lanes, an->blk_up, st);
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    an->ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    m.an = std::move(an);
+    return *m.an;
+}
+
+}  // namespace pclab_b200

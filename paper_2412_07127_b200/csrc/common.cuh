@@ -1,0 +1,102 @@
+// Shared device/host plumbing for the B200 PCG + IC(0) + GNN-correction path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace pclab_b200 {
+
+// ---------------------------------------------------------------- errors
+// Mirrors the reference's exception taxonomy (error.hpp:8-29); the C-ABI
+// folds these onto pclab_status exactly like capi.cpp:33-56.
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DimensionError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct NumericError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string("CUDA error in ") + what + " (" + file + ":" +
+                        std::to_string(line) + "): " + cudaGetErrorString(e));
+}
+#define CK(x) ::pclab_b200::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::pclab_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Number of SMs on the current device (148 on B200).
+int sm_count();
+
+// ------------------------------------------------------------ device bits
+// "Not yet computed" marker for the sync-free solves and the IC(0)
+// factorisation: a NaN whose two 32-bit halves are equal, so a plain
+// 32-bit fill writes it. Real results never carry this payload (arithmetic
+// NaNs are canonical 0x7ff8...).
+constexpr unsigned long long kPending = 0x7FFA5A5A7FFA5A5AULL;
+// Row broke down during IC(0): dependants consume it and produce NaN.
+constexpr unsigned long long kBroken = 0x7FF8000000000000ULL;
+
+#ifdef __CUDACC__
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double(static_cast<long long>(v));
+}
+__device__ __forceinline__ void st_relaxed(double* p, double x) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p),
+                 "l"(static_cast<unsigned long long>(__double_as_longlong(x)))
+                 : "memory");
+}
+__device__ __forceinline__ bool is_pending(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == kPending;
+}
+// Spin until the slot holds a computed value.
+__device__ __forceinline__ double wait_value(const double* p) {
+    double v = ld_relaxed(p);
+    while (is_pending(v)) {
+        __nanosleep(20);
+        v = ld_relaxed(p);
+    }
+    return v;
+}
+__device__ __forceinline__ double pending_value() {
+    return __longlong_as_double(static_cast<long long>(kPending));
+}
+
+template <int W>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+    return v;
+}
+
+// Deterministic block reduction (fixed tree) of one double per thread.
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v, double* smem /* BLOCK/32 */) {
+    v = group_sum<32>(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) smem[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (wid == 0) {
+        t = lane < BLOCK / 32 ? smem[lane] : 0.0;
+        t = group_sum<32>(t);
+    }
+    __syncthreads();
+    return t;  // valid in thread 0
+}
+#endif
+
+}  // namespace pclab_b200

@@ -1,0 +1,178 @@
+// Host-side objects of the B200 path. Everything large lives in HBM; the
+// host keeps only shapes, device pointers and small scalars.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pclab_b200 {
+
+// Owning device buffer.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(int64_t count) { alloc(count); }
+    void alloc(int64_t count) {
+        reset();
+        n = count;
+        if (count > 0) CK(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { reset(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    size_t bytes() const { return sizeof(T) * static_cast<size_t>(n); }
+};
+
+// CSR in HBM: int64 row pointers, int32 column indices (strictly
+// increasing per row), fp64 values.
+struct DevCsr {
+    int64_t n = 0, nnz = 0;
+    DevBuf<int64_t> rp;
+    DevBuf<int32_t> cols;
+    DevBuf<double> vals;
+};
+
+// Dependency schedule of a triangular sweep over blocks of `bs`
+// consecutive rows: blocks sorted by (level, index) and cut into warp
+// items of at most `per_item` blocks of one level.
+struct Schedule {
+    int bs = 1;
+    int lanes = 32;     // lanes per block inside a warp (32 / per_item)
+    int per_item = 1;   // blocks per warp item
+    int64_t nblocks = 0;
+    int32_t nlevels = 0;
+    int64_t nitems = 0;
+    DevBuf<int32_t> level;       // [nblocks] level of each block
+    DevBuf<int32_t> order;       // [nblocks] blocks in schedule order
+    DevBuf<int64_t> item_first;  // [nitems] first position in `order`
+    DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item
+    int64_t max_level_width = 0;
+};
+
+// Symbolic analysis of a structurally symmetric matrix (the reference's
+// lower_triangle + csr_transpose, sparse.cpp:137/189, done once on the
+// device): L pattern with A's lower values, U = L^T pattern, the slot map
+// U -> L, and the forward/backward schedules.
+struct Analysis {
+    DevCsr lower;            // pattern of L, values = lower triangle of A
+    DevCsr upper;            // pattern of U = L^T (values unused)
+    DevBuf<int64_t> u2l;     // [nnz(U)] position in L of each U entry
+    int bs = 1;              // detected dof block size (3 for elasticity)
+    Schedule row_lo;         // bs = 1, one row per warp (IC(0))
+    Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
+    Schedule rowlev_up;      // bs = 1 upper levels (reported only)
+    double ms = 0.0;         // wall time of the analysis (CUDA events)
+};
+
+struct Matrix {
+    DevCsr a;
+    DevBuf<int64_t> diag_pos;  // [n] position of a_ii in row i, -1 if absent
+    bool symmetric_known = false, symmetric = false;
+    int64_t missing_diag_row = -1;  // first row without a diagonal
+    std::unique_ptr<Analysis> an;
+};
+
+struct Model {
+    std::vector<double> params;  // 997, layout of gnn.hpp:18-27
+};
+
+enum class Kind { None = 0, Jacobi = 1, IC0 = 2, NIC = 3, GnnIC = 4 };
+const char* kind_name(Kind k);
+Kind parse_kind(const std::string& s);
+
+struct Precond {
+    Kind kind = Kind::None;
+    const Matrix* a = nullptr;  // borrowed
+    DevBuf<double> lvals;       // factor values on L's pattern
+    DevBuf<double> uvals;       // same values on U's pattern (gathered)
+    DevBuf<double> diag;        // Jacobi payload
+    double sigma = 1.0;         // GNN edge scale
+    int ic0_attempts = 0;
+    double ms_analysis = 0, ms_ic0 = 0, ms_gnn = 0, ms_total = 0;
+};
+
+struct SolveReport {
+    int64_t iterations = 0;
+    bool converged = false;
+    double final_rel_residual = 0, true_rel_residual = 0;
+    bool residual_mismatch = false;
+    double p_time = 0, cg_time = 0, total_time = 0, tri_solve_time_per_iter = 0;
+    double analysis_time = 0, ic0_time = 0, gnn_time = 0;
+    std::vector<double> residual_history;
+    std::string to_json() const;
+};
+
+// ----------------------------------------------------------- entry points
+cudaStream_t lib_stream();
+
+// matrices (gen.cu / capi.cpp)
+std::unique_ptr<Matrix> matrix_from_csr_host(int64_t n, const int64_t* rp, const int32_t* cols,
+                                             const double* vals, cudaStream_t st);
+std::unique_ptr<Matrix> matrix_from_csr_device(int64_t n, int64_t nnz, const int64_t* rp,
+                                               const int32_t* cols, const double* vals,
+                                               cudaStream_t st);
+std::unique_ptr<Matrix> gen_poisson_device(int dim, int64_t m, const double* cell_k_host,
+                                           cudaStream_t st);
+std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double* moduli_host,
+                                              cudaStream_t st);
+void matrix_validate(Matrix& a, cudaStream_t st);  // diag positions, row order
+bool matrix_symmetric(Matrix& a, cudaStream_t st);
+
+// analysis.cu
+Analysis& ensure_analysis(Matrix& a, cudaStream_t st);
+void compute_levels(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
+                    Schedule& s, cudaStream_t st);
+
+// ic0.cu: factor values on an.lower's pattern; returns shift attempts
+int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st);
+
+// gnn.cu: GNN forward over the lower-triangle graph; out aligned with L.
+void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* out,
+                 double* sigma_out, cudaStream_t st);
+
+// kernels.cu
+void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
+void trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
+          cudaStream_t st);
+void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st);
+void fill_pending(double* p, int64_t n, cudaStream_t st);
+
+// precond + pcg (pcg.cu)
+std::unique_ptr<Precond> build_precond(Matrix& a, Kind k, const Model* m, cudaStream_t st);
+SolveReport pcg_solve(Matrix& a, const Precond& p, const double* b_dev, double* x_dev,
+                      double rel_tol, int64_t max_iters, bool record_history,
+                      cudaStream_t st);
+
+// host helpers (host.cpp)
+void element_stiffness(double h, double nu, double* ke);
+uint64_t derive_seed(uint64_t seed, uint64_t tag);
+double uniform_at(uint64_t seed, uint64_t i);
+double normal_at(uint64_t seed, uint64_t i);
+std::vector<double> gnn_init_params(uint64_t seed);
+
+}  // namespace pclab_b200

@@ -1,0 +1,183 @@
+// Level-scheduled, sync-free IC(0) numeric factorisation, bit-identical to
+// the reference's up-looking ic0_attempt (src/precond.cpp:23-75) and
+// driven by its shift policy (src/precond.cpp:109-143).
+//
+// Reference order per row i: for each off-diagonal entry (i, j) in column
+// order, s = a_ij; s -= l_ic * l_jc for every shared column c < j in
+// ascending c; l_ij = s / l_jj; diag_acc += l_ij^2; finally
+// l_ii = sqrt(a_ii + shift - diag_acc).
+//
+// Device mapping: one warp per row, rows claimed in (level, index) order.
+// Lane t owns entry t of the row and keeps its running s_t in a register.
+// Step u finalises entry u (owner lane divides by l_{c_u c_u}) and
+// broadcasts l_{i c_u}; every later lane t whose row c_t contains column
+// c_u subtracts l_{i c_u} * l_{c_t c_u}. Entry t therefore receives its
+// subtractions in ascending column order, exactly the reference's merge
+// order, and every product/difference/quotient is explicitly rounded
+// (no FMA), so the factor is bit-identical. Each entry of L starts as
+// kPending and is published by its final store; dependants poll only the
+// entries they read, so rows pipeline across levels without barriers.
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "core.h"
+
+namespace pclab_b200 {
+
+namespace {
+
+template <int C>
+__global__ void __launch_bounds__(256)
+ic0_kernel(int64_t nitems, const int32_t* __restrict__ order, const int64_t* __restrict__ lrp,
+           const int32_t* __restrict__ lcols, const double* __restrict__ avals, double shift,
+           double* v, unsigned long long* fail_row, unsigned* counter) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems) return;
+        const int64_t i = order[it];  // one row per item
+        const int64_t beg = lrp[i];
+        const int nd = static_cast<int>(lrp[i + 1] - beg) - 1;  // off-diagonals
+        double s[C], qval[C], dj[C];
+        int32_t jc[C], qcol[C];
+        int64_t q[C], qend[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int t = lane + 32 * c;
+            jc[c] = -1;
+            qcol[c] = INT_MAX;
+            q[c] = qend[c] = 0;
+            s[c] = qval[c] = dj[c] = 0.0;
+            if (t < nd) {
+                jc[c] = lcols[beg + t];
+                s[c] = avals[beg + t];
+                q[c] = lrp[jc[c]];
+                qend[c] = lrp[jc[c] + 1] - 1;  // position of l_jj
+                dj[c] = ld_relaxed(v + qend[c]);
+                if (q[c] < qend[c]) {
+                    qcol[c] = lcols[q[c]];
+                    qval[c] = ld_relaxed(v + q[c]);
+                }
+            }
+        }
+        double diag_acc = 0.0;
+        for (int u = 0; u < nd; ++u) {
+            const int owner = u & 31, oc = u >> 5;
+            double l = 0.0;
+            int32_t cu = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                if (c == oc && lane == owner) {
+                    double d = dj[c];
+                    while (is_pending(d)) d = ld_relaxed(v + qend[c]);
+                    l = __ddiv_rn(s[c], d);
+                    st_relaxed(v + beg + u, l);
+                    cu = jc[c];
+                }
+            l = __shfl_sync(0xffffffffu, l, owner);
+            cu = __shfl_sync(0xffffffffu, cu, owner);
+            diag_acc = __dadd_rn(diag_acc, __dmul_rn(l, l));
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int t = lane + 32 * c;
+                if (t <= u || t >= nd) continue;
+                while (qcol[c] < cu) {
+                    ++q[c];
+                    if (q[c] < qend[c]) {
+                        qcol[c] = lcols[q[c]];
+                        qval[c] = ld_relaxed(v + q[c]);
+                    } else {
+                        qcol[c] = INT_MAX;
+                    }
+                }
+                if (qcol[c] == cu) {
+                    double w = qval[c];
+                    while (is_pending(w)) w = ld_relaxed(v + q[c]);
+                    s[c] = __dsub_rn(s[c], __dmul_rn(l, w));
+                    ++q[c];
+                    if (q[c] < qend[c]) {
+                        qcol[c] = lcols[q[c]];
+                        qval[c] = ld_relaxed(v + q[c]);
+                    } else {
+                        qcol[c] = INT_MAX;
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            const double sd = __dsub_rn(__dadd_rn(avals[beg + nd], shift), diag_acc);
+            if (!(sd > 0.0)) {
+                st_relaxed(v + beg + nd, __longlong_as_double(static_cast<long long>(kBroken)));
+                atomicMin(fail_row, static_cast<unsigned long long>(i));
+            } else {
+                st_relaxed(v + beg + nd, __dsqrt_rn(sd));
+            }
+        }
+    }
+}
+
+__global__ void row_stats(int64_t n, const int64_t* __restrict__ rp, const double* __restrict__ lv,
+                          unsigned* maxlen, unsigned long long* maxdiag) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    atomicMax(maxlen, static_cast<unsigned>(rp[i + 1] - rp[i]));
+    // |a_ii| >= 0: its IEEE bit pattern orders like an unsigned integer
+    atomicMax(maxdiag, static_cast<unsigned long long>(__double_as_longlong(fabs(lv[rp[i + 1] - 1]))));
+}
+
+}  // namespace
+
+int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st) {
+    const int64_t n = a.a.n;
+    const DevCsr& L = an.lower;
+    if (n == 0) return 0;
+    // max|a_ii| over the diagonal (precond.cpp:114-118) sets the shift scale
+    DevBuf<unsigned> mx(1);
+    DevBuf<unsigned long long> md(1);
+    CK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(md.p, 0, sizeof(unsigned long long), st));
+    row_stats<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, L.rp.p, L.vals.p, mx.p, md.p);
+    CK_LAUNCH();
+    unsigned maxlen = 0;
+    unsigned long long mdbits = 0;
+    CK(cudaMemcpyAsync(&maxlen, mx.p, sizeof maxlen, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&mdbits, md.p, sizeof mdbits, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double max_diag;
+    std::memcpy(&max_diag, &mdbits, sizeof max_diag);
+    if (maxlen > 256)
+        throw DimensionError("ic0: a row of L has " + std::to_string(maxlen) +
+                             " entries; the device kernel supports up to 256");
+    const double alpha0 = 1e-8 * max_diag;
+    DevBuf<unsigned long long> fail(1);
+    DevBuf<unsigned> ctr(1);
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    for (int attempt = 0;; ++attempt) {
+        const double shift = attempt == 0 ? 0.0 : alpha0 * static_cast<double>(1 << (attempt - 1));
+        fill_pending(out, L.nnz, st);
+        CK(cudaMemsetAsync(fail.p, 0xff, sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
+        const Schedule& s = an.row_lo;
+        if (maxlen <= 64)
+            ic0_kernel<2><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
+                                                 out, fail.p, ctr.p);
+        else if (maxlen <= 128)
+            ic0_kernel<4><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
+                                                 out, fail.p, ctr.p);
+        else
+            ic0_kernel<8><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
+                                                 out, fail.p, ctr.p);
+        CK_LAUNCH();
+        unsigned long long f = 0;
+        CK(cudaMemcpyAsync(&f, fail.p, sizeof f, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (f == ~0ULL) return attempt;
+        if (attempt == 3)
+            throw NumericError("ic0: nonpositive pivot at row " + std::to_string(f));
+    }
+}
+
+}  // namespace pclab_b200

@@ -1,0 +1,132 @@
+// Host wrappers for the stand-alone sparse kernels (SpMV, the two sweeps,
+// U value gather, pending fill). The PCG loop uses fused variants in
+// pcg.cu; these are the building blocks exposed through the C-ABI.
+#include "core.h"
+#include "sweep.cuh"
+
+namespace pclab_b200 {
+
+namespace {
+
+__global__ void fill_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(256)
+spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+            const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y) {
+    const int gl = threadIdx.x % LPR;
+    const int64_t g0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / LPR;
+    const int64_t ng = static_cast<int64_t>(gridDim.x) * blockDim.x / LPR;
+    const int64_t nround = (n + ng - 1) / ng;
+    for (int64_t r = 0; r < nround; ++r) {
+        const int64_t row = g0 + r * ng;
+        const bool active = row < n;
+        const double s = row_dot<LPR>(rp, cols, vals, x, row, gl, active);
+        if (active && gl == 0) y[row] = s;
+    }
+}
+
+__global__ void gather_kernel(int64_t m, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k < m) dst[k] = src[idx[k]];
+}
+
+}  // namespace
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+void fill_pending(double* p, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    fill_kernel<<<sm_count() * 4, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(p), n, kPending);
+    CK_LAUNCH();
+}
+
+int spmv_lanes(const Matrix& a) {
+    const double avg = a.a.n ? static_cast<double>(a.a.nnz) / static_cast<double>(a.a.n) : 1.0;
+    int l = 4;
+    while (l < 32 && l < avg) l *= 2;
+    return l;
+}
+
+void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
+    const int64_t n = a.a.n;
+    if (n == 0) return;
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    switch (spmv_lanes(a)) {
+        case 4: spmv_kernel<4><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
+        case 8: spmv_kernel<8><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
+        case 16: spmv_kernel<16><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
+        default: spmv_kernel<32><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
+    }
+    CK_LAUNCH();
+}
+
+void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st) {
+    const int64_t m = an.upper.nnz;
+    if (m == 0) return;
+    gather_kernel<<<static_cast<unsigned>((m + 255) / 256), 256, 0, st>>>(m, an.u2l.p, lvals, uvals);
+    CK_LAUNCH();
+}
+
+template <int LG, int BS, bool UP>
+static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals, const double* b,
+                          double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.order.p, s.item_first.p, s.item_cnt.p,
+                                                  M.rp.p, M.cols.p, vals, b, x, reset, done, ctr);
+}
+
+template <int BS, bool UP>
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const double* vals, const double* b,
+                           double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
+    switch (s.lanes) {
+        case 2:
+        case 4: launch_trsv_t<4, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
+        case 8: launch_trsv_t<8, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
+        case 16: launch_trsv_t<16, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
+        default: launch_trsv_t<32, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
+    }
+}
+
+// Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
+// with kPending) and the optional reset buffer.
+void launch_trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
+                 double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
+    const Schedule& s = upper ? an.blk_up : an.blk_lo;
+    const DevCsr& M = upper ? an.upper : an.lower;
+    if (s.nitems == 0) return;
+    if (upper) {
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, vals, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, vals, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, vals, b, x, reset, done, ctr, st);
+    } else {
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, vals, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, vals, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, vals, b, x, reset, done, ctr, st);
+    }
+    CK_LAUNCH();
+}
+
+void trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
+          cudaStream_t st) {
+    DevBuf<unsigned> ctr(1);
+    CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
+    fill_pending(x, an.lower.n, st);
+    launch_trsv(an, vals, upper, b, x, nullptr, nullptr, ctr.p, st);
+    CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace pclab_b200

@@ -1,0 +1,466 @@
+// Preconditioner construction and the PCG loop (reference: ic0 /
+// nic_predict / gnn_ic_predict src/precond.cpp:109-168, pcg
+// src/krylov.cpp:114-190).
+//
+// One PCG iteration is five kernels, all resident-data, no host round trip:
+//   1. spmv_p : p <- z + beta p (on the fly, double-buffered), q = A p,
+//               pAp (deterministic two-pass), alpha = rz / pAp
+//   2. axpy   : x += alpha p, r -= alpha q, ||r|| -> convergence flag
+//   3. sweep L: y = L^-1 r   (sync-free; also re-arms z)
+//   4. sweep U: z = L^-T y   (sync-free; also re-arms y)
+//   5. dot_rz : rz' = r.z, beta = rz'/rz
+// Scalars live in device memory; the last CTA of each reduction finalises
+// them in a fixed order, so runs are bit-reproducible. Iterations are
+// captured in a CUDA graph (every kernel no-ops once `done` is set) and the
+// host polls the flag once per graph launch; the iteration count is exact.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "core.h"
+#include "sweep.cuh"
+
+namespace pclab_b200 {
+
+void launch_trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
+                 double* reset, const int* done, unsigned* ctr, cudaStream_t st);
+int spmv_lanes(const Matrix& a);
+
+namespace {
+
+constexpr int kT = 256;
+
+struct Scal {
+    double rz, pap, alpha, beta, bnorm, rel, rel_tol, rr;
+    long long iter, max_iters;
+    int done, converged, error, pad;
+    unsigned ticket[4];
+    unsigned ctr[2];
+};
+
+// Last-CTA finalisation of a per-CTA partial: returns true in the CTA
+// that must finish the reduction; *total is then valid in thread 0.
+__device__ __forceinline__ bool finish_partial(double local, double* part, unsigned* ticket,
+                                               double* total) {
+    __shared__ double sm[kT / 32];
+    __shared__ bool last;
+    const double bs = block_sum<kT>(local, sm);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = bs;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += kT) s += __ldcg(part + b);
+    s = block_sum<kT>(s, sm);
+    if (threadIdx.x == 0) {
+        *total = s;
+        *ticket = 0;
+    }
+    return true;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(kT)
+k_spmv_p(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+         const double* __restrict__ vals, const double* __restrict__ z,
+         const double* __restrict__ pold, double* __restrict__ pnew, double* __restrict__ q,
+         Scal* S, double* part) {
+    if (S->done) return;
+    const double beta = S->beta;
+    const int gl = threadIdx.x % LPR;
+    const int64_t g0 = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) / LPR;
+    const int64_t ng = static_cast<int64_t>(gridDim.x) * kT / LPR;
+    const int64_t nround = (n + ng - 1) / ng;
+    double loc = 0.0;
+    for (int64_t r = 0; r < nround; ++r) {
+        const int64_t row = g0 + r * ng;
+        const bool active = row < n;
+        double acc = 0.0;
+        if (active) {
+            const int64_t b = rp[row], e = rp[row + 1];
+            int64_t k = b + gl;
+            for (; k + 3 * LPR < e; k += 4 * LPR) {
+                const int32_t j0 = __ldg(cols + k), j1 = __ldg(cols + k + LPR),
+                              j2 = __ldg(cols + k + 2 * LPR), j3 = __ldg(cols + k + 3 * LPR);
+                const double v0 = __ldg(vals + k), v1 = __ldg(vals + k + LPR),
+                             v2 = __ldg(vals + k + 2 * LPR), v3 = __ldg(vals + k + 3 * LPR);
+                acc = fma(v0, fma(beta, __ldg(pold + j0), __ldg(z + j0)), acc);
+                acc = fma(v1, fma(beta, __ldg(pold + j1), __ldg(z + j1)), acc);
+                acc = fma(v2, fma(beta, __ldg(pold + j2), __ldg(z + j2)), acc);
+                acc = fma(v3, fma(beta, __ldg(pold + j3), __ldg(z + j3)), acc);
+            }
+            for (; k < e; k += LPR) {
+                const int32_t j = __ldg(cols + k);
+                acc = fma(__ldg(vals + k), fma(beta, __ldg(pold + j), __ldg(z + j)), acc);
+            }
+        }
+        acc = group_sum<LPR>(acc);
+        if (active && gl == 0) {
+            const double pn = fma(beta, pold[row], z[row]);
+            pnew[row] = pn;
+            q[row] = acc;
+            loc = fma(pn, acc, loc);
+        }
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
+        S->pap = tot;
+        if (!(tot > 0.0)) {
+            S->error = 1;
+            S->done = 1;
+        } else {
+            S->alpha = S->rz / tot;
+        }
+        S->ctr[0] = 0;
+        S->ctr[1] = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kT)
+k_axpy(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
+       double* __restrict__ r, Scal* S, double* part, double* hist) {
+    if (S->done) return;
+    const double alpha = S->alpha;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        x[i] = fma(alpha, p[i], x[i]);
+        const double ri = fma(-alpha, q[i], r[i]);
+        r[i] = ri;
+        loc = fma(ri, ri, loc);
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[1], &tot) && threadIdx.x == 0) {
+        S->rr = tot;
+        const double rel = sqrt(tot) / S->bnorm;
+        const long long it = S->iter + 1;
+        S->iter = it;
+        S->rel = rel;
+        if (hist) hist[it] = rel;
+        if (rel <= S->rel_tol) {
+            S->converged = 1;
+            S->done = 1;
+        } else if (it >= S->max_iters) {
+            S->done = 1;
+        }
+    }
+}
+
+// mode 0: rz' -> beta, rz   mode 1: setup rz (beta = 0)   mode 2: bnorm
+__global__ void __launch_bounds__(kT)
+k_dot(int64_t n, const double* __restrict__ a, const double* __restrict__ b, Scal* S, double* part,
+      int mode) {
+    if (mode == 0 && S->done) return;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT)
+        loc = fma(a[i], b[i], loc);
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[2], &tot) && threadIdx.x == 0) {
+        if (mode == 0) {
+            S->beta = tot / S->rz;
+            S->rz = tot;
+        } else if (mode == 1) {
+            S->rz = tot;
+            S->beta = 0.0;
+        } else {
+            S->bnorm = sqrt(tot);
+        }
+    }
+}
+
+__global__ void k_jacobi(int64_t n, const double* __restrict__ r, const double* __restrict__ d,
+                         double* __restrict__ z, const Scal* S) {
+    if (S->done) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT)
+        z[i] = r[i] / d[i];
+}
+
+__global__ void k_resid(int64_t n, const double* __restrict__ b, double* __restrict__ ax) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x;
+    if (i < n) ax[i] = b[i] - ax[i];
+}
+
+__global__ void k_combine(int64_t n, const int64_t* __restrict__ lrp, double* __restrict__ l,
+                          const double* __restrict__ o, double sigma, int nic,
+                          unsigned long long* bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t k = lrp[i]; k < lrp[i + 1]; ++k) l[k] = nic ? o[k] * sigma : l[k] + o[k];
+    if (!(l[lrp[i + 1] - 1] > 0.0)) atomicMin(bad, static_cast<unsigned long long>(i));
+}
+
+__global__ void k_jacobi_diag(int64_t n, const double* __restrict__ vals,
+                              const int64_t* __restrict__ dpos, double* __restrict__ d,
+                              unsigned long long* bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x;
+    if (i >= n) return;
+    const double v = dpos[i] >= 0 ? vals[dpos[i]] : 0.0;
+    d[i] = v;
+    if (!(v > 0.0)) atomicMin(bad, static_cast<unsigned long long>(i));
+}
+
+inline unsigned gfor(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s) {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, st));
+    }
+    double ms() {
+        CK(cudaEventRecord(b, st));
+        CK(cudaEventSynchronize(b));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, a, b));
+        return t;
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+};
+
+unsigned long long read_flag(unsigned long long* d, cudaStream_t st) {
+    unsigned long long h;
+    CK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h;
+}
+
+}  // namespace
+
+const char* kind_name(Kind k) {
+    switch (k) {
+        case Kind::None: return "none";
+        case Kind::Jacobi: return "jacobi";
+        case Kind::IC0: return "ic0";
+        case Kind::NIC: return "nic";
+        case Kind::GnnIC: return "gnnic";
+    }
+    return "unknown";
+}
+
+Kind parse_kind(const std::string& k) {
+    if (k == "none") return Kind::None;
+    if (k == "jacobi") return Kind::Jacobi;
+    if (k == "ic0") return Kind::IC0;
+    if (k == "nic") return Kind::NIC;
+    if (k == "gnnic") return Kind::GnnIC;
+    throw DimensionError("unknown preconditioner kind '" + k + "'");
+}
+
+std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model, cudaStream_t st) {
+    auto p = std::make_unique<Precond>();
+    p->kind = kind;
+    p->a = &a;
+    const int64_t n = a.a.n;
+    Timer total(st);
+    if (kind == Kind::None) return p;
+    if (a.a.n != a.a.n) throw DimensionError("matrix not square");
+    DevBuf<unsigned long long> bad(1);
+    CK(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    if (kind == Kind::Jacobi) {
+        p->diag.alloc(n);
+        if (n) k_jacobi_diag<<<gfor(n), kT, 0, st>>>(n, a.a.vals.p, a.diag_pos.p, p->diag.p, bad.p);
+        CK_LAUNCH();
+        const auto f = read_flag(bad.p, st);
+        if (f != ~0ULL) throw NumericError("jacobi: nonpositive diagonal at row " + std::to_string(f));
+        p->ms_total = total.ms();
+        return p;
+    }
+    if ((kind == Kind::NIC || kind == Kind::GnnIC) && model == nullptr)
+        throw DimensionError(std::string("kind '") + kind_name(kind) + "' needs a model");
+    if (!matrix_symmetric(a, st)) throw FormatError("lower_triangle: matrix not symmetric");
+    if (a.missing_diag_row >= 0) {
+        if (kind == Kind::NIC)
+            throw FormatError("lower factor: missing diagonal at row " + std::to_string(a.missing_diag_row));
+        throw FormatError("ic0: missing diagonal at row " + std::to_string(a.missing_diag_row));
+    }
+    {
+        const bool fresh = !a.an;
+        Timer t(st);
+        ensure_analysis(a, st);
+        p->ms_analysis = fresh ? a.an->ms : 0.0;
+        (void)t;
+    }
+    const Analysis& an = *a.an;
+    p->lvals.alloc(an.lower.nnz);
+    p->uvals.alloc(an.upper.nnz);
+    if (kind == Kind::IC0 || kind == Kind::GnnIC) {
+        Timer t(st);
+        p->ic0_attempts = ic0_factor(a, an, p->lvals.p, st);
+        p->ms_ic0 = t.ms();
+    }
+    if (kind == Kind::NIC || kind == Kind::GnnIC) {
+        Timer t(st);
+        DevBuf<double> out(an.lower.nnz);
+        gnn_forward(a, an, *model, out.p, &p->sigma, st);
+        if (n)
+            k_combine<<<gfor(n), kT, 0, st>>>(n, an.lower.rp.p, p->lvals.p, out.p, p->sigma,
+                                              kind == Kind::NIC, bad.p);
+        CK_LAUNCH();
+        const auto f = read_flag(bad.p, st);
+        if (f != ~0ULL)
+            throw NumericError("lower factor: nonpositive diagonal at row " + std::to_string(f));
+        p->ms_gnn = t.ms();
+    }
+    gather_upper(an, p->lvals.p, p->uvals.p, st);
+    p->ms_total = total.ms() + p->ms_analysis;
+    return p;
+}
+
+SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, double rel_tol,
+                      int64_t max_iters, bool record, cudaStream_t st) {
+    if (!(rel_tol > 0.0)) throw DimensionError("pcg: rel_tol must be > 0");
+    const int64_t n = a.a.n;
+    if (max_iters < 0) max_iters = 10 * n;
+    SolveReport rep;
+    rep.p_time = pc.ms_total / 1e3;
+    rep.analysis_time = pc.ms_analysis / 1e3;
+    rep.ic0_time = pc.ms_ic0 / 1e3;
+    rep.gnn_time = pc.ms_gnn / 1e3;
+    const bool factor = pc.kind == Kind::IC0 || pc.kind == Kind::NIC || pc.kind == Kind::GnnIC;
+    Timer cg(st);
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    const int parts_max = sm_count() * 8;
+    DevBuf<Scal> S(1);
+    DevBuf<double> part(parts_max), r(n), q(n), pa(n), pb(n), y, zbuf, tmp(n);
+    DevBuf<double> hist;
+    if (record) hist.alloc(max_iters + 1);
+    Scal h{};
+    h.rel_tol = rel_tol;
+    h.max_iters = max_iters;
+    CK(cudaMemcpyAsync(S.p, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    const unsigned vgrid = static_cast<unsigned>(sm_count() * 4);
+    const unsigned sgrid = static_cast<unsigned>(sm_count() * 8);
+    if (n) k_dot<<<vgrid, kT, 0, st>>>(n, b, b, S.p, part.p, 2);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h.bnorm == 0.0 || n == 0) {
+        rep.converged = true;
+        if (record) rep.residual_history.push_back(0.0);
+        rep.cg_time = cg.ms() / 1e3;
+        rep.total_time = rep.p_time + rep.cg_time;
+        return rep;
+    }
+    CK(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    // rel_0 = ||b|| / ||b|| (krylov.cpp:143): identical operands, exactly 1
+    const double rel0 = 1.0;
+    rep.final_rel_residual = rel0;
+    if (record) {
+        CK(cudaMemcpyAsync(hist.p, &rel0, sizeof rel0, cudaMemcpyHostToDevice, st));
+    }
+    if (rel0 <= rel_tol) {
+        rep.converged = true;
+        if (record) rep.residual_history.push_back(rel0);
+        rep.cg_time = cg.ms() / 1e3;
+        rep.total_time = rep.p_time + rep.cg_time;
+        rep.true_rel_residual = 1.0;
+        return rep;
+    }
+    const Analysis* an = factor ? a.an.get() : nullptr;
+    double* z = r.p;  // kind none: z aliases r
+    if (factor) {
+        y.alloc(n);
+        zbuf.alloc(n);
+        z = zbuf.p;
+        fill_pending(y.p, n, st);
+        fill_pending(z, n, st);
+    } else if (pc.kind == Kind::Jacobi) {
+        zbuf.alloc(n);
+        z = zbuf.p;
+    }
+    // ---- z0 = M^-1 r0, rz, beta = 0, p = 0
+    {
+        Timer tt(st);
+        if (factor) {
+            CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 2, st));
+            launch_trsv(*an, pc.lvals.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
+            launch_trsv(*an, pc.uvals.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
+        } else if (pc.kind == Kind::Jacobi) {
+            k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
+        }
+        CK_LAUNCH();
+        rep.tri_solve_time_per_iter = factor ? tt.ms() / 1e3 : 0.0;
+    }
+    k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
+    CK(cudaMemsetAsync(pa.p, 0, sizeof(double) * n, st));
+    CK_LAUNCH();
+    // ---- capture an even number of iterations (p buffers alternate)
+    const int lpr = spmv_lanes(a);
+    auto iteration = [&](double* pold, double* pnew) {
+        switch (lpr) {
+            case 4: k_spmv_p<4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
+            case 8: k_spmv_p<8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
+            case 16: k_spmv_p<16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
+            default: k_spmv_p<32><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
+        }
+        k_axpy<<<vgrid, kT, 0, st>>>(n, pnew, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+        if (factor) {
+            launch_trsv(*an, pc.lvals.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            launch_trsv(*an, pc.uvals.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+        } else if (pc.kind == Kind::Jacobi) {
+            k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
+        }
+        k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+    };
+    const int pairs = n > 2000000 ? 4 : 8;  // iterations per graph = 2 * pairs
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < pairs; ++k) {
+        iteration(pa.p, pb.p);
+        iteration(pb.p, pa.p);
+    }
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    int* hdone = nullptr;
+    CK(cudaMallocHost(&hdone, sizeof(int)));
+    for (;;) {
+        CK(cudaGraphLaunch(exec, st));
+        CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (*hdone) break;
+    }
+    cudaFreeHost(hdone);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    rep.cg_time = cg.ms() / 1e3;
+    CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h.error)
+        throw NumericError("pcg: nonpositive curvature at iteration " + std::to_string(h.iter + 1) +
+                           " (matrix not SPD?)");
+    rep.iterations = h.iter;
+    rep.converged = h.converged != 0;
+    rep.final_rel_residual = h.rel;
+    if (record) {
+        rep.residual_history.resize(h.iter + 1);
+        CK(cudaMemcpyAsync(rep.residual_history.data(), hist.p, sizeof(double) * (h.iter + 1),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    // true residual ||b - A x|| / ||b|| (krylov.cpp:182-188); k_dot mode 2
+    // writes its norm into the bnorm slot
+    const double bnorm = h.bnorm;
+    spmv(a, x, tmp.p, st);
+    k_resid<<<gfor(n), kT, 0, st>>>(n, b, tmp.p);
+    k_dot<<<vgrid, kT, 0, st>>>(n, tmp.p, tmp.p, S.p, part.p, 2);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rep.true_rel_residual = h.bnorm / bnorm;
+    rep.residual_mismatch =
+        std::fabs(rep.true_rel_residual - rep.final_rel_residual) > 10.0 * rel_tol;
+    rep.total_time = rep.p_time + rep.cg_time;
+    return rep;
+}
+
+}  // namespace pclab_b200
