@@ -114,6 +114,9 @@ pclab_status pclab_matrix_gen_elasticity(int64_t m, double nu, const double* mod
 /* Copy the CSR back (host or device destinations). */
 pclab_status pclab_matrix_csr(const pclab_matrix* a, int64_t* row_ptr, int32_t* cols,
                               double* vals);
+/* Discard the cached symbolic analysis so the next preconditioner build
+ * redoes it (benchmarks time the full path). */
+pclab_status pclab_matrix_drop_analysis(pclab_matrix* a);
 /* Device pointers of the CSR (no copy). */
 pclab_status pclab_matrix_device_csr(const pclab_matrix* a, const int64_t** row_ptr,
                                      const int32_t** cols, const double** vals);
@@ -147,6 +150,19 @@ pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p,
                                     const double* b, double* x, double rel_tol,
                                     int64_t max_iters, int record_history,
                                     void* stream, char** report_json_out);
+
+/* Per-kernel device times of the PCG loop: runs up to max_iters eager
+ * iterations (rel_tol 1e-300) with a CUDA event between kernels and writes
+ * ms6 = [spmv+p-update, axpy+norm, sweep L, sweep L^T, dot, iterations]. */
+pclab_status pclab_pcg_profile(pclab_matrix* a, const pclab_precond* p, const double* b,
+                               double* x, int64_t max_iters, double* ms6);
+
+/* Run all subsequent library work on `stream` (a cudaStream_t; NULL
+ * restores the library's private stream). */
+void pclab_set_stream(void* stream);
+
+/* Kernel launches issued by the library so far (graph nodes included). */
+long long pclab_launch_count(void);
 
 /* Individual kernels on device vectors. */
 pclab_status pclab_spmv_device(const pclab_matrix* a, const double* x, double* y,

@@ -106,6 +106,10 @@ def lib() -> C.CDLL:
         "pclab_pcg_solve_device": (st, [_vp, _vp, _vp, _vp, C.c_double, C.c_int64, C.c_int, _vp,
                                         C.POINTER(C.c_void_p)]),
         "pclab_spmv_device": (st, [_vp, _vp, _vp, _vp]),
+        "pclab_pcg_profile": (st, [_vp, _vp, _vp, _vp, C.c_int64, _f64p]),
+        "pclab_set_stream": (None, [_vp]),
+        "pclab_matrix_drop_analysis": (st, [_vp]),
+        "pclab_launch_count": (C.c_longlong, []),
         "pclab_trsv_device": (st, [_vp, C.c_int, _vp, _vp, _vp]),
         "pclab_uniform_at": (C.c_double, [C.c_uint64, C.c_uint64]),
         "pclab_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
@@ -248,6 +252,9 @@ class Matrix:
         _check(lib().pclab_matrix_device_csr(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value or 0, b.value or 0, c.value or 0
 
+    def drop_analysis(self):
+        _check(lib().pclab_matrix_drop_analysis(self._h))
+
     def spmv_device(self, x_ptr: int, y_ptr: int, stream: int = 0):
         _check(lib().pclab_spmv_device(self._h, x_ptr, y_ptr, stream or None))
 
@@ -357,6 +364,13 @@ class Precond:
     def trsv_device(self, upper: bool, b_ptr: int, x_ptr: int, stream: int = 0):
         _check(lib().pclab_trsv_device(self._h, int(upper), b_ptr, x_ptr, stream or None))
 
+    def profile_device(self, b_ptr: int, x_ptr: int, iters: int) -> dict:
+        """Per-kernel device ms of the PCG loop (eager iterations)."""
+        t = np.zeros(6)
+        _check(lib().pclab_pcg_profile(self.matrix.handle, self._h, b_ptr, x_ptr, iters, t))
+        return {"spmv_ms": t[0], "axpy_ms": t[1], "sweep_lower_ms": t[2], "sweep_upper_ms": t[3],
+                "dot_ms": t[4], "iterations": int(t[5])}
+
     def solve_device(self, b_ptr: int, x_ptr: int, rel_tol: float = 1e-6, max_iters: int = -1,
                      record_history: bool = False, stream: int = 0) -> dict:
         rep = C.c_void_p()
@@ -375,6 +389,15 @@ def pcg_solve(a: Matrix, b, kind: str = "ic0", model: Optional[Model] = None, re
     _check(lib().pclab_pcg_solve(a.handle, bb, kind.encode(), model.handle if model else None, rel_tol,
                                  max_iters, x, C.byref(rep)))
     return x, json.loads(_take_string(rep))
+
+
+def set_stream(stream: int):
+    """Run all library work on this cudaStream_t (0 = the library's own)."""
+    lib().pclab_set_stream(stream or None)
+
+
+def launch_count() -> int:
+    return int(lib().pclab_launch_count())
 
 
 def run(command: str, config: Optional[dict] = None) -> dict:

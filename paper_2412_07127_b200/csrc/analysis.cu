@@ -71,37 +71,95 @@ __global__ void block_check(int64_t n, int bs, const int64_t* __restrict__ lrp,
         if (lcols[e - 1 - s] != i - s) { *bad = 1; return; }
 }
 
-// Sync-free level computation in natural order: warps grab blocks in
-// ascending (lower) or descending (upper) order, so every dependency was
-// grabbed earlier by a running warp and the spin always terminates.
-template <bool UPPER>
-__global__ void levels_kernel(int64_t nb, int bs, const int64_t* __restrict__ rp,
-                              const int32_t* __restrict__ cols, int32_t* level,
-                              unsigned long long* counter) {
+// Level sets by Kahn layering on the block DAG: a block's level is one
+// more than the largest level among its predecessors, so releasing a block
+// when its last predecessor is processed assigns exactly that level (the
+// frontier order is irrelevant; the schedule is sorted afterwards). One
+// launch per level, replayed from a CUDA graph.
+struct KState {
+    unsigned long long beg, end, tail;
+    int lvl, pad;
+};
+
+__device__ __forceinline__ bool is_pred(int64_t jb, int64_t b, bool upper) {
+    return upper ? jb > b : jb < b;
+}
+
+__global__ void kahn_init(int64_t nb, int bs, const int64_t* __restrict__ prp,
+                          const int32_t* __restrict__ pcols, bool upper, int32_t* __restrict__ indeg,
+                          int32_t* __restrict__ level, int32_t* __restrict__ fr, KState* ks) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    int cnt = 0;
+    for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
+        for (int64_t k = prp[i]; k < prp[i + 1]; ++k) cnt += is_pred(pcols[k] / bs, b, upper);
+    indeg[b] = cnt;
+    level[b] = -1;
+    if (cnt == 0) {
+        level[b] = 0;
+        fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(b);
+    }
+}
+
+// warp per frontier block, lanes over the successor entries
+__global__ void kahn_step(int bs, const int64_t* __restrict__ srp, const int32_t* __restrict__ scols,
+                          bool upper, int32_t* __restrict__ indeg, int32_t* __restrict__ level,
+                          int32_t* __restrict__ fr, KState* ks) {
+    const unsigned long long beg = ks->beg, end = ks->end;
+    const int nl = ks->lvl + 1;
     const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(counter, 1ULL);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= static_cast<unsigned long long>(nb)) return;
-        const int64_t b = UPPER ? nb - 1 - static_cast<int64_t>(t) : static_cast<int64_t>(t);
-        int lv = 0;
+    const unsigned long long w0 = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5;
+    const unsigned long long nw = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
+    for (unsigned long long p = beg + w0; p < end; p += nw) {
+        const int64_t b = fr[p];
         for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
-            for (int64_t k = rp[i] + lane; k < rp[i + 1]; k += 32) {
-                const int64_t jb = cols[k] / bs;
-                if (UPPER ? jb > b : jb < b) {
-                    int v;
-                    do {
-                        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(level + jb) : "memory");
-                    } while (v < 0);
-                    lv = max(lv, v + 1);
+            for (int64_t k = srp[i] + lane; k < srp[i + 1]; k += 32) {
+                const int64_t jb = scols[k] / bs;
+                if (!is_pred(b, jb, upper)) continue;  // b precedes jb
+                if (atomicSub(&indeg[jb], 1) == 1) {
+                    level[jb] = nl;
+                    fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(jb);
                 }
             }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
-        if (lane == 0)
-            asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(level + b), "r"(lv) : "memory");
     }
+}
+
+__global__ void kahn_start(KState* ks) {
+    ks->beg = 0;
+    ks->end = ks->tail;
+    ks->lvl = 0;
+}
+
+__global__ void kahn_advance(KState* ks) {
+    if (ks->end == ks->tail) {
+        ks->beg = ks->end;  // frontier exhausted: stays empty
+        return;
+    }
+    ks->beg = ks->end;
+    ks->end = ks->tail;
+    ks->lvl += 1;
+}
+
+// The dependency a sweep polls first: the predecessor block of highest
+// (level, index); its last-published row is bs - 1.
+__global__ void crit_kernel(int64_t nb, int bs, const int64_t* __restrict__ prp,
+                            const int32_t* __restrict__ pcols, bool upper,
+                            const int32_t* __restrict__ level, int32_t* __restrict__ crit) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    int64_t best = -1;
+    int bl = -1;
+    for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
+        for (int64_t k = prp[i]; k < prp[i + 1]; ++k) {
+            const int64_t jb = pcols[k] / bs;
+            if (!is_pred(jb, b, upper)) continue;
+            const int l = level[jb];
+            if (l > bl || (l == bl && jb > best)) {
+                bl = l;
+                best = jb;
+            }
+        }
+    crit[b] = best < 0 ? -1 : static_cast<int32_t>(best * bs + bs - 1);
 }
 
 __global__ void iota32(int32_t* p, int64_t n) {
@@ -122,6 +180,16 @@ __global__ void items_per_level(int32_t nl, int64_t nb, int per_item,
     if (l >= nl) return;
     const int64_t end = l + 1 < nl ? start[l + 1] : nb;
     nit[l] = (end - start[l] + per_item - 1) / per_item;
+}
+
+__global__ void slots_fill(int64_t nitems, int per_item, const int32_t* __restrict__ order,
+                           const int64_t* __restrict__ first, const int32_t* __restrict__ cnt,
+                           int32_t* __restrict__ slots) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= nitems * per_item) return;
+    const int64_t it = k / per_item;
+    const int g = static_cast<int>(k % per_item);
+    slots[k] = g < cnt[it] ? order[first[it] + g] : -1;
 }
 
 __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* __restrict__ start,
@@ -157,27 +225,53 @@ inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t
 
 }  // namespace
 
-void compute_levels(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
-                    Schedule& s, cudaStream_t st) {
+void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
+                    cudaStream_t st) {
+    const int64_t n = pred.n;
     s.bs = bs;
     s.nblocks = n / bs;
     s.level.alloc(std::max<int64_t>(s.nblocks, 1));
+    s.crit.alloc(std::max<int64_t>(s.nblocks, 1));
     if (s.nblocks == 0) return;
-    CK(cudaMemsetAsync(s.level.p, 0xff, sizeof(int32_t) * s.nblocks, st));
-    DevBuf<unsigned long long> ctr(1);
-    CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned long long), st));
-    const int threads = 256;
-    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
-    if (upper)
-        levels_kernel<true><<<grid, threads, 0, st>>>(s.nblocks, bs, rp, cols, s.level.p, ctr.p);
-    else
-        levels_kernel<false><<<grid, threads, 0, st>>>(s.nblocks, bs, rp, cols, s.level.p, ctr.p);
+    const int64_t nb = s.nblocks;
+    DevBuf<int32_t> indeg(nb), fr(nb);
+    DevBuf<KState> ks(1);
+    CK(cudaMemsetAsync(ks.p, 0, sizeof(KState), st));
+    kahn_init<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, indeg.p, s.level.p,
+                                                 fr.p, ks.p);
+    CK_LAUNCH();
+    kahn_start<<<1, 1, 0, st>>>(ks.p);  // frontier of level 0 = the seeds
+    CK_LAUNCH();
+    const unsigned grid = static_cast<unsigned>(sm_count() * 4);
+    constexpr int kSteps = 32;
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kSteps; ++k) {
+        kahn_step<<<grid, 256, 0, st>>>(bs, succ.rp.p, succ.cols.p, upper, indeg.p, s.level.p, fr.p, ks.p);
+        kahn_advance<<<1, 1, 0, st>>>(ks.p);
+    }
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    KState h{};
+    for (;;) {
+        CK(cudaGraphLaunch(ge, st));
+        CK(cudaMemcpyAsync(&h, ks.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h.beg == h.end) break;
+    }
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    if (h.tail != static_cast<unsigned long long>(nb))
+        throw FormatError("level analysis: dependency graph has a cycle");
+    crit_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, s.level.p,
+                                                   s.crit.p);
     CK_LAUNCH();
 }
 
-static void build_schedule(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
-                           int lanes, Schedule& s, cudaStream_t st) {
-    compute_levels(rp, cols, n, bs, upper, s, st);
+static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, int lanes,
+                           Schedule& s, cudaStream_t st) {
+    compute_levels(pred, succ, bs, upper, s, st);
     s.lanes = lanes;
     s.per_item = 32 / lanes;
     const int64_t nb = s.nblocks;
@@ -220,6 +314,10 @@ static void build_schedule(const int64_t* rp, const int32_t* cols, int64_t n, in
     s.item_cnt.alloc(s.nitems);
     items_fill<<<grid_for(s.nlevels, 128), 128, 0, st>>>(s.nlevels, nb, s.per_item, start.p, nit.p,
                                                         s.item_first.p, s.item_cnt.p);
+    CK_LAUNCH();
+    s.slots.alloc(s.nitems * s.per_item);
+    slots_fill<<<grid_for(s.nitems * s.per_item, 256), 256, 0, st>>>(s.nitems, s.per_item, s.order.p,
+                                                                     s.item_first.p, s.item_cnt.p, s.slots.p);
     CK_LAUNCH();
     CK(cudaStreamSynchronize(st));
 }
@@ -284,9 +382,9 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
           : 0.0;
     int lanes = 2;
     while (lanes < 32 && lanes < off_per_block) lanes *= 2;
-    build_schedule(L.rp.p, L.cols.p, n, 1, false, 32, an->row_lo, st);
-    build_schedule(L.rp.p, L.cols.p, n, bs, false, lanes, an->blk_lo, st);
-    build_schedule(U.rp.p, U.cols.p, n, bs, true, lanes, an->blk_up, st);
+    build_schedule(L, U, 1, false, 32, an->row_lo, st);
+    build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
+    build_schedule(U, L, bs, true, lanes, an->blk_up, st);
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
     float ms = 0;

@@ -31,7 +31,14 @@ struct pclab_precond {
 
 namespace pclab_b200 {
 
+static cudaStream_t g_user_stream = nullptr;
+static bool g_user_stream_set = false;
+
+// The stream every library call runs on: the one set by pclab_set_stream
+// (e.g. the caller's current stream, so its events bracket our work), else
+// a private non-blocking stream.
 cudaStream_t lib_stream() {
+    if (g_user_stream_set) return g_user_stream;
     static cudaStream_t s = [] {
         cudaStream_t t;
         CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
@@ -604,7 +611,7 @@ pclab_status pclab_precond_levels(const pclab_precond* p, int32_t* lo, int32_t* 
         Analysis& an = *m->an;
         cudaStream_t st = lib_stream();
         if (an.rowlev_up.level.n == 0 && an.lower.n > 0)
-            compute_levels(an.upper.rp.p, an.upper.cols.p, an.upper.n, 1, true, an.rowlev_up, st);
+            compute_levels(an.upper, an.lower, 1, true, an.rowlev_up, st);
         CK(cudaStreamSynchronize(st));
         // level counts = 1 + max level (both sweeps)
         auto count = [&](const DevBuf<int32_t>& lv, int64_t n) {
@@ -629,6 +636,31 @@ pclab_status pclab_precond_timings(const pclab_precond* p, double* ms4) {
     ms4[2] = p->p->ms_gnn;
     ms4[3] = p->p->ms_total;
     return PCLAB_OK;
+}
+
+pclab_status pclab_matrix_drop_analysis(pclab_matrix* a) {
+    if (a == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_matrix_drop_analysis: null matrix");
+    return guarded([&] {
+        CK(cudaStreamSynchronize(lib_stream()));
+        a->m->an.reset();
+    });
+}
+
+void pclab_set_stream(void* stream) {
+    g_user_stream = static_cast<cudaStream_t>(stream);
+    g_user_stream_set = stream != nullptr;
+}
+
+long long pclab_launch_count(void) { return launch_count(); }
+
+pclab_status pclab_pcg_profile(pclab_matrix* a, const pclab_precond* p, const double* b, double* x,
+                               int64_t max_iters, double* ms6) {
+    if (a == nullptr || p == nullptr || b == nullptr || x == nullptr || ms6 == nullptr)
+        return fail(PCLAB_ERR_ARGUMENT, "pclab_pcg_profile: null argument");
+    return guarded([&] {
+        if (p->p->a != a->m.get()) throw DimensionError("preconditioner built for another matrix");
+        pcg_solve(*a->m, *p->p, b, x, 1e-300, max_iters, false, lib_stream(), ms6);
+    });
 }
 
 pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p, const double* b, double* x,
@@ -680,7 +712,7 @@ pclab_status pclab_trsv_device(const pclab_precond* p, int upper, const double* 
     return guarded([&] {
         const Analysis* an = p->p->a->an.get();
         if (!an || p->p->lvals.n == 0) throw DimensionError("preconditioner has no factor");
-        trsv(*an, upper ? p->p->uvals.p : p->p->lvals.p, upper != 0, b, x, as_stream(stream));
+        trsv(*an, upper ? p->p->uvals.p : p->p->lvals.p, p->p->invd.p, upper != 0, b, x, as_stream(stream));
     });
 }
 

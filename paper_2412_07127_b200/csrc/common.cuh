@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -33,8 +34,18 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
         throw CudaError(std::string("CUDA error in ") + what + " (" + file + ":" +
                         std::to_string(line) + "): " + cudaGetErrorString(e));
 }
+// Count of kernel launches issued by the library (CK_LAUNCH after each
+// launch; graph replays add their node counts explicitly).
+inline std::atomic<long long> g_launches{0};
+inline void count_launches(long long k) { g_launches += k; }
+inline long long launch_count() { return g_launches.load(); }
+
 #define CK(x) ::pclab_b200::cuda_check((x), #x, __FILE__, __LINE__)
-#define CK_LAUNCH() ::pclab_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define CK_LAUNCH()                                                                         \
+    do {                                                                                    \
+        ::pclab_b200::count_launches(1);                                                    \
+        ::pclab_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+    } while (0)
 
 // Number of SMs on the current device (148 on B200).
 int sm_count();

@@ -68,9 +68,11 @@ struct Schedule {
     int32_t nlevels = 0;
     int64_t nitems = 0;
     DevBuf<int32_t> level;       // [nblocks] level of each block
+    DevBuf<int32_t> crit;        // [nblocks] row polled first (-1: no dependency)
     DevBuf<int32_t> order;       // [nblocks] blocks in schedule order
     DevBuf<int64_t> item_first;  // [nitems] first position in `order`
     DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item
+    DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
     int64_t max_level_width = 0;
 };
 
@@ -110,6 +112,7 @@ struct Precond {
     const Matrix* a = nullptr;  // borrowed
     DevBuf<double> lvals;       // factor values on L's pattern
     DevBuf<double> uvals;       // same values on U's pattern (gathered)
+    DevBuf<double> invd;        // 1 / l_ii (both sweeps)
     DevBuf<double> diag;        // Jacobi payload
     double sigma = 1.0;         // GNN edge scale
     int ic0_attempts = 0;
@@ -145,8 +148,8 @@ bool matrix_symmetric(Matrix& a, cudaStream_t st);
 
 // analysis.cu
 Analysis& ensure_analysis(Matrix& a, cudaStream_t st);
-void compute_levels(const int64_t* rp, const int32_t* cols, int64_t n, int bs, bool upper,
-                    Schedule& s, cudaStream_t st);
+void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
+                    cudaStream_t st);
 
 // ic0.cu: factor values on an.lower's pattern; returns shift attempts
 int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st);
@@ -157,8 +160,13 @@ void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* ou
 
 // kernels.cu
 void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
-void trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
-          cudaStream_t st);
+void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
+          double* x, cudaStream_t st);
+void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper,
+                 const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+                 cudaStream_t st);
+void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);
+int spmv_lanes(const Matrix& a);
 void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st);
 void fill_pending(double* p, int64_t n, cudaStream_t st);
 
@@ -166,7 +174,7 @@ void fill_pending(double* p, int64_t n, cudaStream_t st);
 std::unique_ptr<Precond> build_precond(Matrix& a, Kind k, const Model* m, cudaStream_t st);
 SolveReport pcg_solve(Matrix& a, const Precond& p, const double* b_dev, double* x_dev,
                       double rel_tol, int64_t max_iters, bool record_history,
-                      cudaStream_t st);
+                      cudaStream_t st, double* prof_ms = nullptr);
 
 // host helpers (host.cpp)
 void element_stiffness(double h, double nu, double* ke);

@@ -154,7 +154,12 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
     const double alpha0 = 1e-8 * max_diag;
     DevBuf<unsigned long long> fail(1);
     DevBuf<unsigned> ctr(1);
-    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    // a few levels of rows resident: enough to pipeline, few idle pollers
+    const Schedule& rs = an.row_lo;
+    const double per_level = rs.nlevels ? static_cast<double>(rs.nitems) / rs.nlevels : 1.0;
+    const int64_t blocks = (static_cast<int64_t>(6.0 * per_level) + 8) / 8;
+    const unsigned grid = static_cast<unsigned>(
+        std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
     for (int attempt = 0;; ++attempt) {
         const double shift = attempt == 0 ? 0.0 : alpha0 * static_cast<double>(1 << (attempt - 1));
         fill_pending(out, L.nnz, st);

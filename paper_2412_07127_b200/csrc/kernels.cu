@@ -1,6 +1,11 @@
 // Host wrappers for the stand-alone sparse kernels (SpMV, the two sweeps,
 // U value gather, pending fill). The PCG loop uses fused variants in
 // pcg.cu; these are the building blocks exposed through the C-ABI.
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
 #include "core.h"
 #include "sweep.cuh"
 
@@ -81,52 +86,119 @@ void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaSt
     CK_LAUNCH();
 }
 
+// Developer knob: PCLAB_TRSV_TUNE = mode | (sleep_ns << 8); mode 0 polls the
+// critical predecessor first, mode 1 polls every dependency directly.
+static int trsv_tune() {
+    static const int t = getenv("PCLAB_TRSV_TUNE") ? atoi(getenv("PCLAB_TRSV_TUNE")) : 0;
+    return t;
+}
+// Developer trace (PCLAB_TRSV_TRACE=<file>): per-item globaltimer stamps of
+// the stand-alone sweep, written as int64 [nitems x 4].
+static long long* g_trace = nullptr;
+
+// Resident warps for a sweep: enough to hold a few levels of items in
+// flight (loads stream while the frontier advances) but not so many that
+// idle pollers crowd L2.
+static unsigned trsv_grid(const Schedule& s) {
+    const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
+    static const double depth = getenv("PCLAB_TRSV_DEPTH") ? atof(getenv("PCLAB_TRSV_DEPTH")) : 4.0;
+    const int64_t warps = static_cast<int64_t>(depth * per_level) + 1;
+    const int64_t blocks = (warps + 7) / 8;
+    return static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
+}
+
 template <int LG, int BS, bool UP>
-static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals, const double* b,
-                          double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
-    const unsigned grid = static_cast<unsigned>(sm_count() * 8);
-    trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.order.p, s.item_first.p, s.item_cnt.p,
-                                                  M.rp.p, M.cols.p, vals, b, x, reset, done, ctr);
+static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
+                          const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+                          cudaStream_t st) {
+    trsv_kernel<LG, BS, UP><<<trsv_grid(s), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
+                                                          vals, invd, b, x, reset, done, ctr, trsv_tune(),
+                                                          g_trace);
 }
 
 template <int BS, bool UP>
-static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const double* vals, const double* b,
-                           double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
+                           const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+                           cudaStream_t st) {
     switch (s.lanes) {
         case 2:
-        case 4: launch_trsv_t<4, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
-        case 8: launch_trsv_t<8, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
-        case 16: launch_trsv_t<16, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
-        default: launch_trsv_t<32, BS, UP>(s, M, vals, b, x, reset, done, ctr, st); break;
+        case 4: launch_trsv_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+        case 8: launch_trsv_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+        case 16: launch_trsv_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+        default: launch_trsv_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
     }
 }
 
 // Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
 // with kPending) and the optional reset buffer.
-void launch_trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
-                 double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
+void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper,
+                 const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+                 cudaStream_t st) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, vals, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, vals, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, vals, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, vals, invd, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, vals, invd, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, vals, invd, b, x, reset, done, ctr, st);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, vals, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, vals, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, vals, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, vals, invd, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, vals, invd, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, vals, invd, b, x, reset, done, ctr, st);
     }
     CK_LAUNCH();
 }
 
-void trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
-          cudaStream_t st) {
+void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
+          double* x, cudaStream_t st) {
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
     fill_pending(x, an.lower.n, st);
-    launch_trsv(an, vals, upper, b, x, nullptr, nullptr, ctr.p, st);
+    const char* tf = getenv("PCLAB_TRSV_TRACE");
+    const Schedule& s = upper ? an.blk_up : an.blk_lo;
+    DevBuf<long long> tb;
+    if (tf) {
+        tb.alloc(4 * s.nitems);
+        g_trace = tb.p;
+    }
+    launch_trsv(an, vals, invd, upper, b, x, nullptr, nullptr, ctr.p, st);
     CK(cudaStreamSynchronize(st));
+    g_trace = nullptr;
+    if (tf) {
+        std::vector<long long> h(4 * s.nitems);
+        CK(cudaMemcpy(h.data(), tb.p, tb.bytes(), cudaMemcpyDeviceToHost));
+        std::string path = std::string(tf) + (upper ? ".up" : ".lo");
+        FILE* f = fopen(path.c_str(), "wb");
+        if (f) {
+            fwrite(h.data(), sizeof(long long), h.size(), f);
+            fclose(f);
+        }
+        // levels of the items (block level of the first slot)
+        std::vector<int32_t> lv(s.nblocks), sl(s.nitems * s.per_item);
+        CK(cudaMemcpy(lv.data(), s.level.p, sizeof(int32_t) * s.nblocks, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sl.data(), s.slots.p, sizeof(int32_t) * sl.size(), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> il(s.nitems);
+        for (int64_t i = 0; i < s.nitems; ++i) il[i] = lv[sl[i * s.per_item]];
+        path += ".lev";
+        f = fopen(path.c_str(), "wb");
+        if (f) {
+            fwrite(il.data(), sizeof(int32_t), il.size(), f);
+            fclose(f);
+        }
+    }
+}
+
+__global__ void invd_kernel(int64_t n, const int64_t* __restrict__ lrp, const double* __restrict__ l,
+                            double* __restrict__ invd) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) invd[i] = 1.0 / l[lrp[i + 1] - 1];
+}
+
+void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st) {
+    const int64_t n = an.lower.n;
+    if (n == 0) return;
+    invd_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, an.lower.rp.p, lvals, invd);
+    CK_LAUNCH();
 }
 
 }  // namespace pclab_b200

@@ -22,9 +22,6 @@
 
 namespace pclab_b200 {
 
-void launch_trsv(const Analysis& an, const double* vals, bool upper, const double* b, double* x,
-                 double* reset, const int* done, unsigned* ctr, cudaStream_t st);
-int spmv_lanes(const Matrix& a);
 
 namespace {
 
@@ -312,12 +309,14 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
         p->ms_gnn = t.ms();
     }
     gather_upper(an, p->lvals.p, p->uvals.p, st);
+    p->invd.alloc(n);
+    reciprocal_diag(an, p->lvals.p, p->invd.p, st);
     p->ms_total = total.ms() + p->ms_analysis;
     return p;
 }
 
 SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, double rel_tol,
-                      int64_t max_iters, bool record, cudaStream_t st) {
+                      int64_t max_iters, bool record, cudaStream_t st, double* prof_ms) {
     if (!(rel_tol > 0.0)) throw DimensionError("pcg: rel_tol must be > 0");
     const int64_t n = a.a.n;
     if (max_iters < 0) max_iters = 10 * n;
@@ -383,8 +382,8 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         Timer tt(st);
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 2, st));
-            launch_trsv(*an, pc.lvals.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
-            launch_trsv(*an, pc.uvals.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
+            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
@@ -396,43 +395,87 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK_LAUNCH();
     // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
-    auto iteration = [&](double* pold, double* pnew) {
+    // `mark` runs after each of the five kernels (event hook for profiling)
+    auto iteration_parts = [&](double* pold, double* pnew, auto&& mark) {
         switch (lpr) {
             case 4: k_spmv_p<4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
             case 8: k_spmv_p<8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
             case 16: k_spmv_p<16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
             default: k_spmv_p<32><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
         }
+        mark();
         k_axpy<<<vgrid, kT, 0, st>>>(n, pnew, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+        mark();
         if (factor) {
-            launch_trsv(*an, pc.lvals.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
-            launch_trsv(*an, pc.uvals.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
-        } else if (pc.kind == Kind::Jacobi) {
-            k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            mark();
+            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+            mark();
+        } else {
+            if (pc.kind == Kind::Jacobi) k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
+            mark();
+            mark();
         }
         k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+        mark();
     };
-    const int pairs = n > 2000000 ? 4 : 8;  // iterations per graph = 2 * pairs
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < pairs; ++k) {
-        iteration(pa.p, pb.p);
-        iteration(pb.p, pa.p);
-    }
-    CK(cudaStreamEndCapture(st, &graph));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+    auto iteration = [&](double* pold, double* pnew) { iteration_parts(pold, pnew, [] {}); };
     int* hdone = nullptr;
     CK(cudaMallocHost(&hdone, sizeof(int)));
-    for (;;) {
-        CK(cudaGraphLaunch(exec, st));
-        CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (*hdone) break;
+    if (prof_ms) {
+        // eager iterations with an event between kernels: per-kernel device
+        // times [spmv_p, axpy, sweep L, sweep U, dot] averaged over iterations
+        constexpr int kK = 5;
+        cudaEvent_t ev[kK + 1];
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        double acc[kK] = {0, 0, 0, 0, 0};
+        int done_iters = 0;
+        double* pold = pa.p;
+        double* pnew = pb.p;
+        for (;;) {
+            int k = 0;
+            CK(cudaEventRecord(ev[k++], st));
+            iteration_parts(pold, pnew, [&] { CK(cudaEventRecord(ev[k++], st)); });
+            CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (*hdone) break;  // converged inside: the partial iteration is not counted
+            for (int t = 0; t < kK; ++t) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, ev[t], ev[t + 1]));
+                acc[t] += ms;
+            }
+            ++done_iters;
+            std::swap(pold, pnew);
+        }
+        for (int t = 0; t < kK; ++t) prof_ms[t] = done_iters ? acc[t] / done_iters : 0.0;
+        prof_ms[kK] = done_iters;
+        for (auto& e : ev) cudaEventDestroy(e);
+    } else {
+        const int pairs = n > 2000000 ? 4 : 8;  // iterations per graph = 2 * pairs
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        const long long before = launch_count();
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < pairs; ++k) {
+            iteration(pa.p, pb.p);
+            iteration(pb.p, pa.p);
+        }
+        CK(cudaStreamEndCapture(st, &graph));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        size_t nodes = 0;
+        CK(cudaGraphGetNodes(graph, nullptr, &nodes));
+        g_launches = before;  // captured launches are counted per replay below
+        for (;;) {
+            CK(cudaGraphLaunch(exec, st));
+            count_launches(static_cast<long long>(nodes));
+            CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (*hdone) break;
+        }
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
     }
     cudaFreeHost(hdone);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
     rep.cg_time = cg.ms() / 1e3;
     CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
