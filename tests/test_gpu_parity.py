@@ -93,7 +93,9 @@ def test_gnn_corrected_factor(w):
         ref = O.factor(oa, kind, op)
         assert max_rel(pc.factor(), ref) < 1e-5, kind
     _, sigma = O.gnn_forward(oa, op)
-    assert abs(P.Precond(a, "gnnic", model).info()["sigma"] - sigma) <= 1e-13 * sigma
+    # sd of the lower values: a deterministic tree sum on the device vs the
+    # reference's sequential sum -- equal up to reassociation
+    assert abs(P.Precond(a, "gnnic", model).info()["sigma"] - sigma) <= 1e-11 * sigma
 
 
 @pytest.mark.parametrize("w", SMALL, ids=IDS)
