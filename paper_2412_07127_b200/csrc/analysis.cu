@@ -8,11 +8,14 @@
 // dependency DAG of each sweep is levelled so that warps can run it
 // sync-free in topological order.
 #include <cub/device/device_radix_sort.cuh>
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 
 #include "core.h"
 
 namespace pclab_b200 {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -121,6 +124,46 @@ __global__ void kahn_step(int bs, const int64_t* __restrict__ srp, const int32_t
                     fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(jb);
                 }
             }
+    }
+}
+
+// All levels in one cooperative launch: process the frontier, grid barrier,
+// thread 0 advances the frontier window, grid barrier.
+__global__ void kahn_persistent(int bs, const int64_t* __restrict__ srp,
+                                const int32_t* __restrict__ scols, bool upper,
+                                int32_t* __restrict__ indeg, int32_t* __restrict__ level,
+                                int32_t* __restrict__ fr, KState* ks) {
+    cg::grid_group g = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const unsigned long long w0 = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) >> 5;
+    const unsigned long long nw = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
+    volatile KState* vk = ks;
+    for (;;) {
+        const unsigned long long beg = vk->beg, end = vk->end;
+        if (beg == end) return;
+        const int nl = vk->lvl + 1;
+        for (unsigned long long p = beg + w0; p < end; p += nw) {
+            const int64_t b = __ldcg(fr + p);  // appended by other CTAs: bypass L1
+            for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
+                for (int64_t k = srp[i] + lane; k < srp[i + 1]; k += 32) {
+                    const int64_t jb = scols[k] / bs;
+                    if (!is_pred(b, jb, upper)) continue;
+                    if (atomicSub(&indeg[jb], 1) == 1) {
+                        level[jb] = nl;
+                        fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(jb);
+                    }
+                }
+        }
+        g.sync();
+        if (g.thread_rank() == 0) {
+            const unsigned long long t = vk->tail;
+            vk->beg = end;
+            if (t != end) {
+                vk->end = t;
+                vk->lvl = nl;
+            }
+        }
+        g.sync();
     }
 }
 
@@ -242,26 +285,27 @@ void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, 
     CK_LAUNCH();
     kahn_start<<<1, 1, 0, st>>>(ks.p);  // frontier of level 0 = the seeds
     CK_LAUNCH();
-    const unsigned grid = static_cast<unsigned>(sm_count() * 4);
-    constexpr int kSteps = 32;
-    cudaGraph_t g;
-    cudaGraphExec_t ge;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < kSteps; ++k) {
-        kahn_step<<<grid, 256, 0, st>>>(bs, succ.rp.p, succ.cols.p, upper, indeg.p, s.level.p, fr.p, ks.p);
-        kahn_advance<<<1, 1, 0, st>>>(ks.p);
+    // one cooperative persistent launch: a grid barrier per level instead
+    // of a kernel launch per level
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kahn_persistent, 256, 0));
+    const unsigned grid = static_cast<unsigned>(sm_count() * std::max(1, std::min(per_sm, 4)));
+    {
+        int bs_ = bs;
+        const int64_t* srp = succ.rp.p;
+        const int32_t* scols = succ.cols.p;
+        bool up = upper;
+        int32_t* ind = indeg.p;
+        int32_t* lev = s.level.p;
+        int32_t* frp = fr.p;
+        KState* ksp = ks.p;
+        void* args[] = {&bs_, &srp, &scols, &up, &ind, &lev, &frp, &ksp};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kahn_persistent), grid, 256, args, 0, st));
+        CK_LAUNCH();
     }
-    CK(cudaStreamEndCapture(st, &g));
-    CK(cudaGraphInstantiate(&ge, g, 0));
     KState h{};
-    for (;;) {
-        CK(cudaGraphLaunch(ge, st));
-        CK(cudaMemcpyAsync(&h, ks.p, sizeof h, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (h.beg == h.end) break;
-    }
-    cudaGraphExecDestroy(ge);
-    cudaGraphDestroy(g);
+    CK(cudaMemcpyAsync(&h, ks.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     if (h.tail != static_cast<unsigned long long>(nb))
         throw FormatError("level analysis: dependency graph has a cycle");
     crit_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, s.level.p,

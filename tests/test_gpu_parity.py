@@ -105,6 +105,8 @@ def chaotic(w, kind):
     elasticity. They are held to a band, not to +-1."""
     if w.family == "elasticity":
         return kind in ("none", "jacobi", "gnnic", "nic")
+    if w.log10_hi - w.log10_lo > 2:  # 10^6 coefficient contrast
+        return kind in ("none", "nic")
     return kind == "nic"
 
 
