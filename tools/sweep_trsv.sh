@@ -1,5 +1,7 @@
-for d in 4 16; do
-  echo "DEPTH=$d"
-  PCLAB_TRSV_DEPTH=$d timeout 120 python tools/prof_stages.py elasticity_q1_40 0 30 2>&1 | grep -E "trsv|pcg\[ic0"
-  PCLAB_TRSV_DEPTH=$d PCLAB_TRSV_TRACE=gpurun_out/tr$d python tools/run_kernels.py elasticity_q1_40 0 1 > /dev/null 2>&1; python tools/trace_trsv.py gpurun_out/tr$d | grep -E "items|per item|deltas|L1:|L2:|L3:"
+for cfg in "32 4" "32 8" "16 4"; do
+  set -- $cfg
+  echo "LANES=$1 DEPTH=$2"
+  PCLAB_SWEEP=0 PCLAB_LANES=$1 PCLAB_TRSV_DEPTH=$2 timeout 300 python tools/prof_stages.py elasticity_q1_118 0 10 2>&1 | grep -E "trsv"
 done
+PCLAB_SWEEP=0 timeout 300 python tools/prof_stages.py elasticity_q1_40 0 10 2>&1 | grep -E "trsv"
+PCLAB_SWEEP=0 python tools/gpu_probe.py 2>&1 | grep -E " its |ERR|bitexact" | tail -6
