@@ -61,8 +61,12 @@ void fill_pending(double* p, int64_t n, cudaStream_t st) {
 
 int spmv_lanes(const Matrix& a) {
     const double avg = a.a.n ? static_cast<double>(a.a.nnz) / static_cast<double>(a.a.n) : 1.0;
-    int l = 4;
-    while (l < 32 && l < avg) l *= 2;
+    // Few lanes per row, many rows per warp: on the 81-entry elasticity rows
+    // 4 lanes x 8 loads in flight beat 8/16/32 lanes (measured, configs[2]:
+    // 1.04 vs 1.09/1.25/1.18 ms). Code 5 = 4 lanes with 8 loads per round.
+    int l = avg > 48 ? 5 : 4;
+    if (avg > 200) l = 32;
+    if (getenv("PCLAB_SPMV_LPR")) l = atoi(getenv("PCLAB_SPMV_LPR"));
     return l;
 }
 
@@ -71,7 +75,8 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
     if (n == 0) return;
     const unsigned grid = static_cast<unsigned>(sm_count() * 8);
     switch (spmv_lanes(a)) {
-        case 4: spmv_kernel<4><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
+        case 4:
+        case 5: spmv_kernel<4><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
         case 8: spmv_kernel<8><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
         case 16: spmv_kernel<16><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
         default: spmv_kernel<32><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;

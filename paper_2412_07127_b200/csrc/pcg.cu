@@ -59,14 +59,24 @@ __device__ __forceinline__ bool finish_partial(double local, double* part, unsig
     return true;
 }
 
-template <int LPR>
+// p <- z + beta p (beta from the previous dot; 0 on the first iteration)
 __global__ void __launch_bounds__(kT)
-k_spmv_p(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
-         const double* __restrict__ vals, const double* __restrict__ z,
-         const double* __restrict__ pold, double* __restrict__ pnew, double* __restrict__ q,
-         Scal* S, double* part) {
+k_pupdate(int64_t n, const double* __restrict__ z, double* __restrict__ p, const Scal* S) {
     if (S->done) return;
     const double beta = S->beta;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT)
+        p[i] = fma(beta, p[i], z[i]);
+}
+
+// q = A p and pAp. Lane groups of LPR lanes per row; every index and value
+// load of a row (up to 4 LPR entries) is issued before the first gather.
+template <int LPR, int U>
+__global__ void __launch_bounds__(kT)
+k_spmv_pap(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+           const double* __restrict__ vals, const double* __restrict__ p, double* __restrict__ q,
+           Scal* S, double* part) {
+    if (S->done) return;
     const int gl = threadIdx.x % LPR;
     const int64_t g0 = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) / LPR;
     const int64_t ng = static_cast<int64_t>(gridDim.x) * kT / LPR;
@@ -78,28 +88,24 @@ k_spmv_p(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ 
         double acc = 0.0;
         if (active) {
             const int64_t b = rp[row], e = rp[row + 1];
-            int64_t k = b + gl;
-            for (; k + 3 * LPR < e; k += 4 * LPR) {
-                const int32_t j0 = __ldg(cols + k), j1 = __ldg(cols + k + LPR),
-                              j2 = __ldg(cols + k + 2 * LPR), j3 = __ldg(cols + k + 3 * LPR);
-                const double v0 = __ldg(vals + k), v1 = __ldg(vals + k + LPR),
-                             v2 = __ldg(vals + k + 2 * LPR), v3 = __ldg(vals + k + 3 * LPR);
-                acc = fma(v0, fma(beta, __ldg(pold + j0), __ldg(z + j0)), acc);
-                acc = fma(v1, fma(beta, __ldg(pold + j1), __ldg(z + j1)), acc);
-                acc = fma(v2, fma(beta, __ldg(pold + j2), __ldg(z + j2)), acc);
-                acc = fma(v3, fma(beta, __ldg(pold + j3), __ldg(z + j3)), acc);
-            }
-            for (; k < e; k += LPR) {
-                const int32_t j = __ldg(cols + k);
-                acc = fma(__ldg(vals + k), fma(beta, __ldg(pold + j), __ldg(z + j)), acc);
+            for (int64_t k0 = b + gl; k0 < e; k0 += U * LPR) {
+                int32_t j[U];
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t k = k0 + u * LPR;
+                    j[u] = k < e ? __ldg(cols + k) : -1;
+                    v[u] = k < e ? __ldg(vals + k) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (j[u] >= 0) acc = fma(v[u], __ldg(p + j[u]), acc);
             }
         }
         acc = group_sum<LPR>(acc);
         if (active && gl == 0) {
-            const double pn = fma(beta, pold[row], z[row]);
-            pnew[row] = pn;
             q[row] = acc;
-            loc = fma(pn, acc, loc);
+            loc = fma(p[row], acc, loc);
         }
     }
     double tot;
@@ -397,15 +403,21 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
     // `mark` runs after each of the five kernels (event hook for profiling)
-    auto iteration_parts = [&](double* pold, double* pnew, auto&& mark) {
+    auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
+        k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
         switch (lpr) {
-            case 4: k_spmv_p<4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
-            case 8: k_spmv_p<8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
-            case 16: k_spmv_p<16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
-            default: k_spmv_p<32><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, z, pold, pnew, q.p, S.p, part.p); break;
+            case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 9: k_spmv_pap<8, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 5: k_spmv_pap<4, 8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 3: k_spmv_pap<4, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 2: k_spmv_pap<2, 16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 17: k_spmv_pap<16, 3><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            case 16: k_spmv_pap<16, 6><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+            default: k_spmv_pap<32, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
         }
         mark();
-        k_axpy<<<vgrid, kT, 0, st>>>(n, pnew, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+        k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
         mark();
         if (factor) {
             launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
@@ -446,7 +458,6 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
                 acc[t] += ms;
             }
             ++done_iters;
-            std::swap(pold, pnew);
         }
         for (int t = 0; t < kK; ++t) prof_ms[t] = done_iters ? acc[t] / done_iters : 0.0;
         prof_ms[kK] = done_iters;
@@ -458,8 +469,8 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         const long long before = launch_count();
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < pairs; ++k) {
-            iteration(pa.p, pb.p);
-            iteration(pb.p, pa.p);
+            iteration(pa.p, nullptr);
+            iteration(pa.p, nullptr);
         }
         CK(cudaStreamEndCapture(st, &graph));
         CK(cudaGraphInstantiate(&exec, graph, 0));

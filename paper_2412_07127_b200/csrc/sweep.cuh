@@ -14,22 +14,23 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp,
                                           const double* __restrict__ vals,
                                           const double* __restrict__ x, int64_t row, int gl,
                                           bool active) {
+    constexpr int U = LPR <= 4 ? 8 : (LPR == 16 ? 6 : 4);  // loads of a row batch issued before the gathers
     double acc = 0.0;
     if (active) {
         const int64_t b = rp[row], e = rp[row + 1];
-        int64_t k = b + gl;
-        // 4 independent loads in flight per lane per round
-        for (; k + 3 * LPR < e; k += 4 * LPR) {
-            const int32_t j0 = __ldg(cols + k), j1 = __ldg(cols + k + LPR),
-                          j2 = __ldg(cols + k + 2 * LPR), j3 = __ldg(cols + k + 3 * LPR);
-            const double v0 = __ldg(vals + k), v1 = __ldg(vals + k + LPR),
-                         v2 = __ldg(vals + k + 2 * LPR), v3 = __ldg(vals + k + 3 * LPR);
-            acc = fma(v0, __ldg(x + j0), acc);
-            acc = fma(v1, __ldg(x + j1), acc);
-            acc = fma(v2, __ldg(x + j2), acc);
-            acc = fma(v3, __ldg(x + j3), acc);
+        for (int64_t k0 = b + gl; k0 < e; k0 += U * LPR) {
+            int32_t j[U];
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t k = k0 + u * LPR;
+                j[u] = k < e ? __ldg(cols + k) : -1;
+                v[u] = k < e ? __ldg(vals + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (j[u] >= 0) acc = fma(v[u], __ldg(x + j[u]), acc);
         }
-        for (; k < e; k += LPR) acc = fma(__ldg(vals + k), __ldg(x + __ldg(cols + k)), acc);
     }
     return group_sum<LPR>(acc);
 }

@@ -1,7 +1,14 @@
-for cfg in "32 4" "32 8" "16 4"; do
-  set -- $cfg
-  echo "LANES=$1 DEPTH=$2"
-  PCLAB_SWEEP=0 PCLAB_LANES=$1 PCLAB_TRSV_DEPTH=$2 timeout 300 python tools/prof_stages.py elasticity_q1_118 0 10 2>&1 | grep -E "trsv"
+for l in 5 3 2; do
+ echo LPR=$l; PCLAB_SPMV_LPR=$l python -c "
+import sys; sys.path.insert(0,'.')
+import torch, paper_2412_07127_b200 as P
+w=P.workloads.CONFIGS[2]; a,b,m=P.workloads.build(w); pc=P.Precond(a,'ic0')
+bt=torch.from_numpy(b).cuda(); xt=torch.zeros_like(bt)
+print(pc.profile_device(bt.data_ptr(), xt.data_ptr(), 20))
+x = torch.randn(a.n, dtype=torch.float64, device='cuda'); y=torch.empty_like(x)
+a.spmv_device(x.data_ptr(), y.data_ptr()); torch.cuda.synchronize()
+import time; t=time.perf_counter()
+for _ in range(10): a.spmv_device(x.data_ptr(), y.data_ptr())
+torch.cuda.synchronize(); print('plain spmv ms', (time.perf_counter()-t)/10*1e3)
+"
 done
-PCLAB_SWEEP=0 timeout 300 python tools/prof_stages.py elasticity_q1_40 0 10 2>&1 | grep -E "trsv"
-PCLAB_SWEEP=0 python tools/gpu_probe.py 2>&1 | grep -E " its |ERR|bitexact" | tail -6
