@@ -4,6 +4,11 @@
 
 #include "common.cuh"
 
+// minimum resident 256-thread blocks per SM for the warp sweep (register cap)
+#ifndef TRSV_MINB
+#define TRSV_MINB 4
+#endif
+
 namespace pclab_b200 {
 
 // Rows per warp = 32 / LPR; each lane group of LPR lanes reduces one row
@@ -41,22 +46,27 @@ struct SweepMeta {
     int64_t blk;  // -1: idle lane group
     int64_t rp[BS + 1];
     int32_t crit;
+    double rhs[BS];  // right-hand side of the block (loaded one item ahead)
 };
 
 template <int BS>
 __device__ __forceinline__ SweepMeta<BS> sweep_meta(unsigned it, int64_t nitems, int G, int grp,
                                                     const int32_t* __restrict__ slots,
                                                     const int32_t* __restrict__ crit,
-                                                    const int64_t* __restrict__ rp) {
+                                                    const int64_t* __restrict__ rp, const double* rhs) {
     SweepMeta<BS> m;
     m.blk = it < nitems ? static_cast<int64_t>(__ldg(slots + static_cast<int64_t>(it) * G + grp)) : -1;
     m.crit = -1;
 #pragma unroll
     for (int t = 0; t <= BS; ++t) m.rp[t] = 0;
+#pragma unroll
+    for (int t = 0; t < BS; ++t) m.rhs[t] = 0.0;
     if (m.blk >= 0) {
         m.crit = __ldg(crit + m.blk);
 #pragma unroll
         for (int t = 0; t <= BS; ++t) m.rp[t] = __ldg(rp + m.blk * BS + t);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) m.rhs[t] = rhs[m.blk * BS + t];
     }
     return m;
 }
@@ -82,7 +92,7 @@ __device__ __forceinline__ SweepMeta<BS> sweep_meta(unsigned it, int64_t nitems,
 //   lower (L, row-sorted, diagonal last):  rows r0..r0+BS-1 forward
 //   upper (U = L^T, diagonal first):       rows r0+BS-1..r0 backward
 template <int LG, int BS, bool UPPER>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, TRSV_MINB)
 trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __restrict__ crit,
             const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
             const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs,
@@ -107,8 +117,8 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
     }
     it = __shfl_sync(0xffffffffu, it, 0);
     next = __shfl_sync(0xffffffffu, next, 0);
-    SweepMeta<BS> m = sweep_meta<BS>(it, nitems, G, grp, slots, crit, rp);
-    SweepMeta<BS> mn = sweep_meta<BS>(next, nitems, G, grp, slots, crit, rp);
+    SweepMeta<BS> m = sweep_meta<BS>(it, nitems, G, grp, slots, crit, rp, rhs);
+    SweepMeta<BS> mn = sweep_meta<BS>(next, nitems, G, grp, slots, crit, rp, rhs);
     while (it < nitems) {
         if (mn.blk >= 0) {
             // prefetch the next item's rows: 128-byte lines of values and indices
@@ -117,6 +127,7 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
             for (int64_t a = (e0 & ~31LL) + 32 * gl; a < e1; a += 32 * LG)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + a));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + mn.blk * BS));
         }
         unsigned after = 0;
         if (lane == 0) after = atomicAdd(counter, 1u);
@@ -162,7 +173,7 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
         if (active && gl == 0) {
 #pragma unroll
             for (int t = 0; t < BS; ++t) {
-                brhs[t] = rhs[r0 + t];
+                brhs[t] = m.rhs[t];  // loaded with the metadata, one item ahead
                 binv[t] = __ldg(invd + r0 + t);
             }
             int q = 0;
@@ -263,7 +274,7 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
         it = next;
         m = mn;
         next = after;
-        mn = sweep_meta<BS>(after, nitems, G, grp, slots, crit, rp);
+        mn = sweep_meta<BS>(after, nitems, G, grp, slots, crit, rp, rhs);
     }
 }
 
