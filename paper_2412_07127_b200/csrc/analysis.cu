@@ -35,24 +35,26 @@ __global__ void lu_fill(int64_t n, const int64_t* __restrict__ rp, const int32_t
                         const int64_t* __restrict__ lrp, int32_t* __restrict__ lcols,
                         double* __restrict__ lvals, const int64_t* __restrict__ urp,
                         int32_t* __restrict__ ucols) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    // warp per row, lanes over the entries (coalesced copies)
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= n) return;
-    int64_t o = lrp[i];
-    for (int64_t k = rp[i]; k <= dpos[i]; ++k, ++o) {
-        lcols[o] = cols[k];
-        lvals[o] = vals[k];
+    const int64_t b = rp[i], d = dpos[i], e = rp[i + 1], lo = lrp[i], uo = urp[i];
+    for (int64_t k = b + lane; k <= d; k += 32) {
+        lcols[lo + (k - b)] = cols[k];
+        lvals[lo + (k - b)] = vals[k];
     }
-    o = urp[i];
-    for (int64_t k = dpos[i]; k < rp[i + 1]; ++k, ++o) ucols[o] = cols[k];
+    for (int64_t k = d + lane; k < e; k += 32) ucols[uo + (k - d)] = cols[k];
 }
 
 // u2l[t]: U entry (i, j), j >= i, is L entry (j, i) in row j.
 __global__ void u2l_fill(int64_t n, const int64_t* __restrict__ urp,
                          const int32_t* __restrict__ ucols, const int64_t* __restrict__ lrp,
                          const int32_t* __restrict__ lcols, int64_t* __restrict__ u2l) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= n) return;
-    for (int64_t t = urp[i]; t < urp[i + 1]; ++t) {
+    for (int64_t t = urp[i] + lane; t < urp[i + 1]; t += 32) {
         const int32_t j = ucols[t];
         int64_t lo = lrp[j], hi = lrp[j + 1];
         while (lo < hi) {
@@ -562,11 +564,11 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     U.cols.alloc(U.nnz);
     an->u2l.alloc(U.nnz);
     if (n > 0) {
-        lu_fill<<<grid_for(n, 256), 256, 0, st>>>(n, a.rp.p, a.cols.p, a.vals.p, m.diag_pos.p,
-                                                  L.rp.p, L.cols.p, L.vals.p, U.rp.p, U.cols.p);
+        lu_fill<<<grid_for(n * 32, 256), 256, 0, st>>>(n, a.rp.p, a.cols.p, a.vals.p, m.diag_pos.p,
+                                                       L.rp.p, L.cols.p, L.vals.p, U.rp.p, U.cols.p);
         CK_LAUNCH();
-        u2l_fill<<<grid_for(n, 256), 256, 0, st>>>(n, U.rp.p, U.cols.p, L.rp.p, L.cols.p,
-                                                   an->u2l.p);
+        u2l_fill<<<grid_for(n * 32, 256), 256, 0, st>>>(n, U.rp.p, U.cols.p, L.rp.p, L.cols.p,
+                                                        an->u2l.p);
         CK_LAUNCH();
     }
     // dof block size: the largest bs in {3, 2} whose diagonal blocks are
@@ -592,7 +594,7 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     int lanes = 2;
     while (lanes < 32 && lanes < off_per_block) lanes *= 2;
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
-    build_schedule(L, U, 1, false, 32, an->row_lo, st);
+    // (row-granular level sets are computed on request only: pclab_precond_levels)
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
     build_schedule(U, L, bs, true, lanes, an->blk_up, st);
     // chunked / TMA-fed sweeps (experimental, PCLAB_SWEEP=1|2): their

@@ -34,6 +34,29 @@ namespace pclab_b200 {
 static cudaStream_t g_user_stream = nullptr;
 static bool g_user_stream_set = false;
 
+void* dev_alloc(size_t bytes) {
+    static bool pool_ready = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ULL;  // never hand freed blocks back to the driver
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return true;
+    }();
+    (void)pool_ready;
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, bytes, lib_stream());
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+        CK(e);
+    }
+    return p;
+}
+
+void dev_free(void* p) { cudaFreeAsync(p, lib_stream()); }
+
 // The stream every library call runs on: the one set by pclab_set_stream
 // (e.g. the caller's current stream, so its events bracket our work), else
 // a private non-blocking stream.
@@ -125,7 +148,15 @@ char* dup_string(const std::string& s) {
     return p;
 }
 
-cudaStream_t as_stream(void* s) { return s ? static_cast<cudaStream_t>(s) : lib_stream(); }
+// A stream passed to a device entry point becomes the library stream, so
+// stream-ordered temporaries and the kernels that use them share one order.
+cudaStream_t as_stream(void* s) {
+    if (s) {
+        g_user_stream = static_cast<cudaStream_t>(s);
+        g_user_stream_set = true;
+    }
+    return lib_stream();
+}
 
 std::string entry_str(int64_t i, int64_t j) {
     return "(" + std::to_string(i) + ", " + std::to_string(j) + ")";
@@ -610,6 +641,8 @@ pclab_status pclab_precond_levels(const pclab_precond* p, int32_t* lo, int32_t* 
         if (!m->an) throw DimensionError("preconditioner has no factor");
         Analysis& an = *m->an;
         cudaStream_t st = lib_stream();
+        if (an.row_lo.level.n == 0 && an.lower.n > 0)
+            compute_levels(an.lower, an.upper, 1, false, an.row_lo, st);
         if (an.rowlev_up.level.n == 0 && an.lower.n > 0)
             compute_levels(an.upper, an.lower, 1, true, an.rowlev_up, st);
         CK(cudaStreamSynchronize(st));

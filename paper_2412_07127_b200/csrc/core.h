@@ -17,7 +17,13 @@ namespace pclab_b200 {
 // Largest row chunk of the chunked sweeps (its values live in shared memory).
 constexpr int64_t kMaxChunkRows = 6144;
 
-// Owning device buffer.
+cudaStream_t lib_stream();
+void* dev_alloc(size_t bytes);  // stream-ordered on lib_stream(), pooled
+void dev_free(void* p);
+
+// Owning device buffer. Allocation and release are stream-ordered on the
+// library stream (cudaMallocAsync from a pool that keeps its memory), so
+// temporaries never force a device-wide synchronisation.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -27,10 +33,10 @@ struct DevBuf {
     void alloc(int64_t count) {
         reset();
         n = count;
-        if (count > 0) CK(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+        if (count > 0) p = static_cast<T*>(dev_alloc(sizeof(T) * static_cast<size_t>(count)));
     }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         n = 0;
     }

@@ -29,16 +29,25 @@ namespace {
 
 template <int C>
 __global__ void __launch_bounds__(256)
-ic0_kernel(int64_t nitems, const int32_t* __restrict__ order, const int64_t* __restrict__ lrp,
-           const int32_t* __restrict__ lcols, const double* __restrict__ avals, double shift,
-           double* v, unsigned long long* fail_row, unsigned* counter) {
+ic0_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict__ slots,
+           const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
+           const double* __restrict__ avals, double shift, double* v, unsigned long long* fail_row,
+           unsigned* counter) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned it = 0;
         if (lane == 0) it = atomicAdd(counter, 1u);
         it = __shfl_sync(0xffffffffu, it, 0);
-        if (it >= nitems) return;
-        const int64_t i = order[it];  // one row per item
+        if (it >= nitems * bs) return;
+        // claim v = item * bs + t: row t of every block of the item. Rows t of
+        // a block are claimed right after rows 0..t-1 (a topological order),
+        // by different warps, so the in-block chain pipelines entry by entry.
+        const int64_t item = it / bs;
+        const int t_row = static_cast<int>(it % bs);
+    for (int g = 0; g < per_item; ++g) {
+        const int32_t blk = slots[item * per_item + g];
+        if (blk < 0) continue;
+        const int64_t i = static_cast<int64_t>(blk) * bs + t_row;
         const int64_t beg = lrp[i];
         const int nd = static_cast<int>(lrp[i + 1] - beg) - 1;  // off-diagonals
         double s[C], qval[C], dj[C];
@@ -116,6 +125,8 @@ ic0_kernel(int64_t nitems, const int32_t* __restrict__ order, const int64_t* __r
                 st_relaxed(v + beg + nd, __dsqrt_rn(sd));
             }
         }
+        __syncwarp();
+    }  // rows of the item
     }
 }
 
@@ -155,8 +166,9 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
     DevBuf<unsigned long long> fail(1);
     DevBuf<unsigned> ctr(1);
     // a few levels of rows resident: enough to pipeline, few idle pollers
-    const Schedule& rs = an.row_lo;
-    const double per_level = rs.nlevels ? static_cast<double>(rs.nitems) / rs.nlevels : 1.0;
+    // the forward-sweep block schedule: a warp per item, rows in order
+    const Schedule& s = an.blk_lo;
+    const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
     const int64_t blocks = (static_cast<int64_t>(6.0 * per_level) + 8) / 8;
     const unsigned grid = static_cast<unsigned>(
         std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
@@ -165,16 +177,15 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
         fill_pending(out, L.nnz, st);
         CK(cudaMemsetAsync(fail.p, 0xff, sizeof(unsigned long long), st));
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
-        const Schedule& s = an.row_lo;
         if (maxlen <= 64)
-            ic0_kernel<2><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
-                                                 out, fail.p, ctr.p);
+            ic0_kernel<2><<<grid, 256, 0, st>>>(s.nitems, s.per_item, s.bs, s.slots.p, L.rp.p, L.cols.p,
+                                                 L.vals.p, shift, out, fail.p, ctr.p);
         else if (maxlen <= 128)
-            ic0_kernel<4><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
-                                                 out, fail.p, ctr.p);
+            ic0_kernel<4><<<grid, 256, 0, st>>>(s.nitems, s.per_item, s.bs, s.slots.p, L.rp.p, L.cols.p,
+                                                 L.vals.p, shift, out, fail.p, ctr.p);
         else
-            ic0_kernel<8><<<grid, 256, 0, st>>>(s.nitems, s.order.p, L.rp.p, L.cols.p, L.vals.p, shift,
-                                                 out, fail.p, ctr.p);
+            ic0_kernel<8><<<grid, 256, 0, st>>>(s.nitems, s.per_item, s.bs, s.slots.p, L.rp.p, L.cols.p,
+                                                 L.vals.p, shift, out, fail.p, ctr.p);
         CK_LAUNCH();
         unsigned long long f = 0;
         CK(cudaMemcpyAsync(&f, fail.p, sizeof f, cudaMemcpyDeviceToHost, st));

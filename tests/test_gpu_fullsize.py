@@ -63,3 +63,33 @@ def test_config1_gnn_factor():
     xo, ro = O.pcg(oa, ob, "ic0", rel_tol=1e-8)
     assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 1
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_config3_ic0_breakdown_row_matches_oracle():
+    """configs[3] (10.06M dofs, lognormal(0, 1.5) moduli): IC(0) breaks down
+    after the reference's three diagonal shifts; the device reports the same
+    first failing row as the oracle (= the reference, bit for bit)."""
+    w = P.workloads.CONFIGS[3]
+    a, b, model = P.workloads.build(w)
+    with pytest.raises(P.NumericError) as dev:
+        P.Precond(a, "ic0")
+    del a
+    oa, ob, op = P.workloads.build_oracle(w)
+    with pytest.raises(O.OracleError) as ref:
+        O.ic0(oa)
+    row = str(ref.value).split("row ")[-1]
+    assert str(dev.value) == f"ic0: nonpositive pivot at row {row}"
+
+
+def test_config4_scaled_gnnic_converges_like_oracle():
+    """configs[4] family (10^u, u ~ U[-3,3], FV diffusion) at 40^3: the
+    GNN-corrected IC(0) converges; iteration count within +-1, solution
+    within 1e-8 relative of the oracle."""
+    w = P.workloads.CONFIGS[4].scaled(40)
+    a, b, model = P.workloads.build(w)
+    oa, ob, op = P.workloads.build_oracle(w)
+    x, rep = P.pcg_solve(a, b, "gnnic", model, rel_tol=1e-8, max_iters=5000)
+    xo, ro = O.pcg(oa, ob, "gnnic", op, rel_tol=1e-8, max_iters=5000)
+    assert rep["converged"] and ro["converged"]
+    assert abs(rep["iterations"] - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
