@@ -78,6 +78,29 @@ __global__ void block_check(int64_t n, int bs, const int64_t* __restrict__ lrp,
         if (lcols[e - 1 - s] != i - s) { *bad = 1; return; }
 }
 
+// Node-blocked off-block pattern: the BS rows of every block reference the
+// same set of whole BS-wide column blocks (row t of block b holds, past its
+// in-block entries, columns BS*k .. BS*k+BS-1 for each neighbour k, in
+// order). Checked on L; U = L^T inherits it.
+__global__ void bsr_check(int64_t nb, int bs, const int64_t* __restrict__ lrp,
+                          const int32_t* __restrict__ lcols, int* __restrict__ bad) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t r0 = b * bs;
+    const int64_t cnt = lrp[r0 + 1] - 1 - lrp[r0];  // off-block entries of row 0
+    if (cnt % bs) { *bad = 1; return; }
+    for (int t = 0; t < bs; ++t) {
+        const int64_t beg = lrp[r0 + t];
+        if (lrp[r0 + t + 1] - (t + 1) - beg != cnt) { *bad = 1; return; }
+        for (int64_t k = 0; k < cnt; k += bs) {
+            const int32_t c0 = lcols[lrp[r0] + k];
+            if (c0 % bs) { *bad = 1; return; }
+            for (int c = 0; c < bs; ++c)
+                if (lcols[beg + k + c] != c0 + c) { *bad = 1; return; }
+        }
+    }
+}
+
 // Level sets by Kahn layering on the block DAG: a block's level is one
 // more than the largest level among its predecessors, so releasing a block
 // when its last predecessor is processed assigns exactly that level (the
@@ -591,8 +614,18 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
         n ? (static_cast<double>(L.nnz) - static_cast<double>(n / bs) * bs * (bs + 1) / 2.0) /
                 static_cast<double>(n / bs)
           : 0.0;
+    an->bsr = false;
+    if (bs > 1 && !(getenv("PCLAB_BSR") && atoi(getenv("PCLAB_BSR")) == 0)) {
+        DevBuf<int> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        bsr_check<<<grid_for(n / bs, 256), 256, 0, st>>>(n / bs, bs, L.rp.p, L.cols.p, bad.p);
+        CK_LAUNCH();
+        an->bsr = dev_read(bad.p, st) == 0;
+    }
+    // node-blocked: one lane per neighbour block; else one per entry
+    const double work = an->bsr ? off_per_block / (bs * bs) : off_per_block;
     int lanes = 2;
-    while (lanes < 32 && lanes < off_per_block) lanes *= 2;
+    while (lanes < 32 && lanes < work) lanes *= 2;
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
     // (row-granular level sets are computed on request only: pclab_precond_levels)
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);

@@ -70,6 +70,31 @@ __device__ __forceinline__ void st_relaxed(double* p, double x) {
                  "l"(static_cast<unsigned long long>(__double_as_longlong(x)))
                  : "memory");
 }
+// Streaming loads of matrix data (read once per sweep/SpMV): evict-first in
+// L2 so the solution vectors the dependency gathers read stay resident.
+#ifdef PCLAB_NO_EVICT_HINT
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldg(p); }
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldg(p); }
+#else
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "ld.global.nc.L2::cache_hint.f64 %0, [%1], pol;\n\t}"
+        : "=d"(v)
+        : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+    int32_t v;
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "ld.global.nc.L2::cache_hint.s32 %0, [%1], pol;\n\t}"
+        : "=r"(v)
+        : "l"(p));
+    return v;
+}
+#endif
 __device__ __forceinline__ bool is_pending(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v)) == kPending;
 }

@@ -103,6 +103,7 @@ struct Analysis {
     DevCsr upper;            // pattern of U = L^T (values unused)
     DevBuf<int64_t> u2l;     // [nnz(U)] position in L of each U entry
     int bs = 1;              // detected dof block size (3 for elasticity)
+    bool bsr = false;        // off-block pattern made of whole bs x bs blocks
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)

@@ -104,9 +104,12 @@ static long long* g_trace = nullptr;
 // Resident warps for a sweep: enough to hold a few levels of items in
 // flight (loads stream while the frontier advances) but not so many that
 // idle pollers crowd L2.
-static unsigned trsv_grid(const Schedule& s) {
+// Measured on configs[2]: 4 levels for the entry-lane sweep, 2 for the
+// node-blocked one (its pollers read BS values each, 1.40 vs 1.65 ms at 4).
+static unsigned trsv_grid(const Schedule& s, double depth_default) {
     const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
-    static const double depth = getenv("PCLAB_TRSV_DEPTH") ? atof(getenv("PCLAB_TRSV_DEPTH")) : 4.0;
+    static const double env_depth = getenv("PCLAB_TRSV_DEPTH") ? atof(getenv("PCLAB_TRSV_DEPTH")) : 0.0;
+    const double depth = env_depth > 0 ? env_depth : depth_default;
     const int64_t warps = static_cast<int64_t>(depth * per_level) + 1;
     const int64_t blocks = (warps + 7) / 8;
     return static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
@@ -116,9 +119,18 @@ template <int LG, int BS, bool UP>
 static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
                           const double* b, double* x, double* reset, const int* done, unsigned* ctr,
                           cudaStream_t st) {
-    trsv_kernel<LG, BS, UP><<<trsv_grid(s), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
+    trsv_kernel<LG, BS, UP><<<trsv_grid(s, 4.0), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
                                                           vals, invd, b, x, reset, done, ctr, trsv_tune(),
                                                           g_trace);
+}
+
+template <int LG, int BS, bool UP>
+static void launch_bsr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
+                         const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+                         cudaStream_t st) {
+    bsr_trsv_kernel<LG, BS, UP><<<trsv_grid(s, 2.0), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
+                                                              vals, invd, b, x, reset, done, ctr, trsv_tune(),
+                                                              g_trace);
 }
 
 // PCLAB_SWEEP=0 selects the warp-item sweep (global level order), default
@@ -173,8 +185,8 @@ static void launch_tma_t(const Schedule& s, const unsigned char* pack, const dou
 }
 
 template <int BS, bool UP>
-static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
-                           const unsigned char* pack, const double* b, double* x, double* reset,
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool bsr, const double* vals,
+                           const double* invd, const unsigned char* pack, const double* b, double* x, double* reset,
                            const int* done, unsigned* ctr, cudaStream_t st) {
     if (sweep_mode() == 2 && pack && s.nchunks > 0 && s.pack_max_item <= kSlotBytes) {
         switch (s.lanes) {
@@ -196,6 +208,18 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const double* val
         }
         return;
     }
+    if constexpr (BS > 1) {
+        if (bsr) {
+            switch (s.lanes) {
+            case 2:
+            case 4: launch_bsr_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+            default: launch_bsr_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+            }
+            return;
+        }
+    }
     switch (s.lanes) {
         case 2:
         case 4: launch_trsv_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
@@ -214,13 +238,13 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, con
     const DevCsr& M = upper ? an.upper : an.lower;
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
     }
     CK_LAUNCH();
 }
@@ -255,12 +279,18 @@ void trsv(const Analysis& an, const double* vals, const double* invd, const unsi
         CK(cudaMemcpy(sl.data(), s.slots.p, sizeof(int32_t) * sl.size(), cudaMemcpyDeviceToHost));
         std::vector<int32_t> il(s.nitems);
         for (int64_t i = 0; i < s.nitems; ++i) il[i] = lv[sl[i * s.per_item]];
-        path += ".lev";
-        f = fopen(path.c_str(), "wb");
-        if (f) {
-            fwrite(il.data(), sizeof(int32_t), il.size(), f);
-            fclose(f);
-        }
+        std::vector<int32_t> cr(s.nblocks);
+        CK(cudaMemcpy(cr.data(), s.crit.p, sizeof(int32_t) * s.nblocks, cudaMemcpyDeviceToHost));
+        auto dump = [&](const std::string& p, const std::vector<int32_t>& v) {
+            FILE* g = fopen(p.c_str(), "wb");
+            if (g) {
+                fwrite(v.data(), sizeof(int32_t), v.size(), g);
+                fclose(g);
+            }
+        };
+        dump(path + ".lev", il);
+        dump(path + ".slots", sl);
+        dump(path + ".crit", cr);
     }
 }
 

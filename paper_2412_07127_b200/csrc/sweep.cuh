@@ -163,8 +163,8 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
                             t = s + 1;
                         }
                     tt[c] = t;
-                    jj[c] = __ldg(cols + ob[t] + e);
-                    v[c] = __ldg(vals + ob[t] + e);
+                    jj[c] = ld_stream(cols + ob[t] + e);
+                    v[c] = ld_stream(vals + ob[t] + e);
                 }
             }
         };
@@ -181,8 +181,8 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
             for (int t = 0; t < BS; ++t)
 #pragma unroll
                 for (int s = 0; s < BS; ++s) {
-                    if (!UPPER && s < t) bin[q++] = __ldg(vals + m.rp[t + 1] - (t + 1) + s);
-                    if (UPPER && s > t) bin[q++] = __ldg(vals + m.rp[t] + (s - t));
+                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + m.rp[t + 1] - (t + 1) + s);
+                    if (UPPER && s > t) bin[q++] = ld_stream(vals + m.rp[t] + (s - t));
                 }
         }
         // (2) one poller per block on the critical predecessor
@@ -202,6 +202,7 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = 0.0;
         const int tmax = __reduce_max_sync(0xffffffffu, total);
+        int rounds = 0;
         for (int base = 0; base < tmax; base += LG * CH) {
             if (base > 0) load_chunk(base);
             double xv[CH];
@@ -211,6 +212,7 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
 #pragma unroll
             for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
             while (__any_sync(0xffffffffu, pend)) {
+                ++rounds;
                 if (sleep_ns) __nanosleep(sleep_ns);
                 pend = false;
 #pragma unroll
@@ -226,6 +228,8 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
                 for (int t = 0; t < BS; ++t)
                     if (tt[c] == t) acc[t] = fma(v[c], xv[c], acc[t]);
         }
+        long long trg = 0;
+        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
         after = __shfl_sync(0xffffffffu, after, 0);
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
@@ -265,12 +269,177 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
             trace[4LL * it + 0] = tr0;
             trace[4LL * it + 1] = tr1;
             trace[4LL * it + 2] = tr2;
-            trace[4LL * it + 3] = smid;
+            (void)smid;
+            trace[4LL * it + 3] = (trg - tr1) * 1024 + min(rounds, 1023);  // gather ns | re-poll rounds
         }
         __syncwarp();
         if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
         // the next item's metadata is fetched only after publication, so its
         // dependent loads never sit on this item's critical path
+        it = next;
+        m = mn;
+        next = after;
+        mn = sweep_meta<BS>(after, nitems, G, grp, slots, crit, rp, rhs);
+    }
+}
+
+// Node-blocked sweep (Analysis::bsr: the off-block pattern is made of
+// whole BSxBS blocks shared by the block's BS rows -- elasticity, where the
+// dofs of a node couple to every dof of each neighbour node). Lane n of the
+// block's LG lanes owns neighbour block n: it streams the BSxBS values and
+// polls the neighbour's BS solution values directly, so the load that
+// observes a dependency's publication is also its gather (no critical-
+// predecessor poll followed by a second L2 round trip), and a neighbour's
+// values are read once instead of once per row.
+//
+// Measured on configs[2] (traces, tools/trace_trsv.py): deeper claim
+// pipelines (3 items per warp) and next-item operands held in registers
+// both start items earlier but lengthen every item's load chain, net
+// slower (1.50 / 1.92 ms vs 1.40 ms per sweep).
+template <int LG, int BS, bool UPPER>
+__global__ void __launch_bounds__(256, TRSV_MINB)
+bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __restrict__ crit,
+                const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs,
+                double* out, double* reset, const int* __restrict__ done, unsigned* counter, int tune,
+                long long* trace) {
+    if (done && *done) return;
+    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+    constexpr int G = 32 / LG;
+    constexpr int NIB = BS * (BS - 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    unsigned it = 0, next = 0;
+    if (lane == 0) {
+        it = atomicAdd(counter, 1u);
+        next = atomicAdd(counter, 1u);
+    }
+    it = __shfl_sync(0xffffffffu, it, 0);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    SweepMeta<BS> m = sweep_meta<BS>(it, nitems, G, grp, slots, crit, rp, rhs);
+    SweepMeta<BS> mn = sweep_meta<BS>(next, nitems, G, grp, slots, crit, rp, rhs);
+    while (it < nitems) {
+        if (mn.blk >= 0) {
+            const int64_t e0 = mn.rp[0], e1 = mn.rp[BS];
+            for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
+            for (int64_t a = (e0 & ~31LL) + 32 * gl; a < e1; a += 32 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + a));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + mn.blk * BS));
+        }
+        unsigned after = 0;
+        if (lane == 0) after = atomicAdd(counter, 1u);
+        long long tr0 = 0;
+        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+        const bool active = m.blk >= 0;
+        const int64_t r0 = active ? m.blk * BS : 0;
+        // off-block entries of row t start at ob[t]; nb neighbour blocks
+        int64_t ob[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? m.rp[t] + (BS - t) : m.rp[t];
+        const int nb = active ? static_cast<int>((UPPER ? m.rp[1] - ob[0] : m.rp[1] - 1 - m.rp[0]) / BS) : 0;
+        double brhs[BS], binv[BS], bin[NIB > 0 ? NIB : 1];
+        if (active && gl == 0) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) {
+                brhs[t] = m.rhs[t];
+                binv[t] = __ldg(invd + r0 + t);
+            }
+            int q = 0;
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int s = 0; s < BS; ++s) {
+                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + m.rp[t + 1] - (t + 1) + s);
+                    if (UPPER && s > t) bin[q++] = ld_stream(vals + m.rp[t] + (s - t));
+                }
+        }
+        double acc[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
+        int rounds = 0;
+        for (int n0 = 0; n0 < nbmax; n0 += LG) {
+            const int n = n0 + gl;
+            const bool own = n < nb;
+            double a[BS][BS], xv[BS];
+            int32_t xc = 0;
+            if (own) {
+                xc = ld_stream(cols + ob[0] + BS * n);
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) a[t][c] = ld_stream(vals + ob[t] + BS * n + c);
+#pragma unroll
+                for (int c = 0; c < BS; ++c) xv[c] = ld_relaxed(out + xc + c);
+            } else {
+#pragma unroll
+                for (int t = 0; t < BS; ++t) {
+                    xv[t] = 0.0;
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
+                }
+            }
+            bool pend = false;
+#pragma unroll
+            for (int c = 0; c < BS; ++c) pend |= own && is_pending(xv[c]);
+            while (__any_sync(0xffffffffu, pend)) {
+                ++rounds;
+                if (sleep_ns) __nanosleep(sleep_ns);
+                pend = false;
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+                    if (own && is_pending(xv[c])) {
+                        xv[c] = ld_relaxed(out + xc + c);
+                        pend |= is_pending(xv[c]);
+                    }
+            }
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+        }
+        long long trg = 0;
+        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
+        after = __shfl_sync(0xffffffffu, after, 0);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+        if (active && gl == 0) {
+            double xb[BS];
+            if (!UPPER) {
+                int q = 0;
+#pragma unroll
+                for (int t = 0; t < BS; ++t) {
+                    double s = brhs[t] - acc[t];
+#pragma unroll
+                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            } else {
+#pragma unroll
+                for (int t = BS - 1; t >= 0; --t) {
+                    double s = brhs[t] - acc[t];
+                    int q = 0;
+#pragma unroll
+                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
+#pragma unroll
+                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+        }
+        if (trace && lane == 0) {
+            long long tr2;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
+            trace[4LL * it + 0] = tr0;
+            trace[4LL * it + 1] = trg;  // no separate critical poll: values in hand
+            trace[4LL * it + 2] = tr2;
+            trace[4LL * it + 3] = min(rounds, 1023);
+        }
+        __syncwarp();
+        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
         it = next;
         m = mn;
         next = after;
