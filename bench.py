@@ -230,20 +230,33 @@ def run_b200(args, w):
     nl = info["nnz_lower"]
     sweep_bytes = 12 * nl + 8 * (n + 1) + 4 * 8 * n  # L vals+cols, row_ptr, rhs, x, 1/l_ii, reset
     spmv_bytes = 12 * nnz + 8 * (n + 1) + 5 * 8 * n  # A vals+cols, row_ptr, z,p_old read, p,q write
-    sweep_ms = prof["sweep_lower_ms"]
-    kern = {
-        "sweep_lower": {"ms": sweep_ms, "bytes": sweep_bytes, "gbs": sweep_bytes / sweep_ms / 1e6},
-        "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": sweep_bytes,
-                        "gbs": sweep_bytes / prof["sweep_upper_ms"] / 1e6},
-        "spmv_p": {"ms": prof["spmv_ms"], "bytes": spmv_bytes, "gbs": spmv_bytes / prof["spmv_ms"] / 1e6},
-        "axpy_norm": {"ms": prof["axpy_ms"], "bytes": 6 * 8 * n, "gbs": 6 * 8 * n / prof["axpy_ms"] / 1e6},
-        "dot": {"ms": prof["dot_ms"], "bytes": 2 * 8 * n, "gbs": 2 * 8 * n / prof["dot_ms"] / 1e6},
-    }
-    iter_bytes = sum(k["bytes"] for k in kern.values()) + sweep_bytes  # both sweeps
+    if prof["fused"]:
+        # backward sweep + w = A z in one kernel; then p, q <- (z, w) + beta (p, q)
+        fused_bytes = sweep_bytes + 12 * nnz + 8 * (n + 1) + 8 * n  # + A vals+cols, row_ptr, w write
+        kern = {
+            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": sweep_bytes},
+            "sweep_upper_spmv": {"ms": prof["sweep_upper_ms"], "bytes": fused_bytes},
+            "pq_update": {"ms": prof["spmv_ms"], "bytes": 6 * 8 * n},
+            "axpy_norm": {"ms": prof["axpy_ms"], "bytes": 6 * 8 * n},
+            "dot": {"ms": prof["dot_ms"], "bytes": 2 * 8 * n},
+        }
+        top, top_name = "sweep_upper_spmv", "bsr_trsv_kernel<upper, fused A z>"
+    else:
+        kern = {
+            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": sweep_bytes},
+            "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": sweep_bytes},
+            "spmv_p": {"ms": prof["spmv_ms"], "bytes": spmv_bytes},
+            "axpy_norm": {"ms": prof["axpy_ms"], "bytes": 6 * 8 * n},
+            "dot": {"ms": prof["dot_ms"], "bytes": 2 * 8 * n},
+        }
+        top, top_name = "sweep_lower", "trsv_kernel (lower sweep)"
+    for k in kern.values():
+        k["gbs"] = k["bytes"] / k["ms"] / 1e6
+    iter_bytes = sum(k["bytes"] for k in kern.values())
     iter_ms = sum(k["ms"] for k in kern.values())
-    achieved = sweep_bytes / sweep_ms / 1e6
+    achieved = kern[top]["gbs"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": "trsv_kernel (lower sweep)",
+                "frac": achieved / hbm, "traffic": None, "kernel": top_name,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "iteration": {"bytes": iter_bytes, "ms": iter_ms, "gbs": iter_bytes / iter_ms / 1e6,
                               "frac": iter_bytes / iter_ms / 1e6 / hbm}}

@@ -153,9 +153,11 @@ pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p,
 
 /* Per-kernel device times of the PCG loop: runs up to max_iters eager
  * iterations (rel_tol 1e-300) with a CUDA event between kernels and writes
- * ms6 = [spmv+p-update, axpy+norm, sweep L, sweep L^T, dot, iterations]. */
+ * ms8 = [k0, axpy+norm, sweep L, k3, dot, iterations, fused, 0] where
+ * fused = 0: k0 = p-update + A p (+ pAp), k3 = sweep L^T;
+ * fused = 1: k0 = p/q update + pq, k3 = sweep L^T fused with w = A z. */
 pclab_status pclab_pcg_profile(pclab_matrix* a, const pclab_precond* p, const double* b,
-                               double* x, int64_t max_iters, double* ms6);
+                               double* x, int64_t max_iters, double* ms8);
 
 /* Run all subsequent library work on `stream` (a cudaStream_t; NULL
  * restores the library's private stream). */

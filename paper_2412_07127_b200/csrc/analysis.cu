@@ -101,6 +101,40 @@ __global__ void bsr_check(int64_t nb, int bs, const int64_t* __restrict__ lrp,
     }
 }
 
+// Same property on the full matrix A (every row of block b holds whole
+// BS-wide column blocks, the same set for its BS rows).
+__global__ void bsr_check_full(int64_t nb, int bs, const int64_t* __restrict__ arp,
+                               const int32_t* __restrict__ acols, int* __restrict__ bad) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t r0 = b * bs;
+    const int64_t cnt = arp[r0 + 1] - arp[r0];
+    if (cnt % bs) { *bad = 1; return; }
+    for (int t = 0; t < bs; ++t) {
+        const int64_t beg = arp[r0 + t];
+        if (arp[r0 + t + 1] - beg != cnt) { *bad = 1; return; }
+        for (int64_t k = 0; k < cnt; k += bs) {
+            const int32_t c0 = acols[arp[r0] + k];
+            if (c0 % bs) { *bad = 1; return; }
+            for (int c = 0; c < bs; ++c)
+                if (acols[beg + k + c] != c0 + c) { *bad = 1; return; }
+        }
+    }
+}
+
+// Key of A block row b for the fused product: the highest backward-sweep
+// level among its column blocks (when its last z input is published).
+__global__ void mv_keys(int64_t nb, int bs, const int32_t* __restrict__ lev, const int64_t* __restrict__ arp,
+                        const int32_t* __restrict__ acols, int32_t* __restrict__ key, int32_t* __restrict__ val) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    int lm = 0;
+    const int64_t r = b * bs;
+    for (int64_t k = arp[r]; k < arp[r + 1]; k += bs) lm = max(lm, lev[acols[k] / bs]);
+    key[b] = lm;
+    val[b] = static_cast<int32_t>(b);
+}
+
 // Level sets by Kahn layering on the block DAG: a block's level is one
 // more than the largest level among its predecessors, so releasing a block
 // when its last predecessor is processed assigns exactly that level (the
@@ -260,6 +294,16 @@ __global__ void slots_fill(int64_t nitems, int per_item, const int32_t* __restri
     const int64_t it = k / per_item;
     const int g = static_cast<int>(k % per_item);
     slots[k] = g < cnt[it] ? order[first[it] + g] : -1;
+}
+
+// Row pointers of every slot's block, stored with the schedule so an
+// item's first dependent load is its entries (node-blocked sweep).
+__global__ void slot_rp_fill(int64_t nslots, int bs, const int32_t* __restrict__ slots,
+                             const int64_t* __restrict__ rp, int64_t* __restrict__ srp) {
+    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (k >= nslots) return;
+    const int32_t b = slots[k];
+    for (int t = 0; t <= bs; ++t) srp[k * (bs + 1) + t] = b >= 0 ? rp[static_cast<int64_t>(b) * bs + t] : 0;
 }
 
 __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* __restrict__ start,
@@ -556,6 +600,24 @@ static void build_chunk_schedule(const DevCsr& pred, int bs, bool upper, int64_t
     }
 }
 
+// A block rows sorted by the backward-sweep level that completes their z
+// inputs (Analysis::mv_order).
+static void build_mv_order(const DevCsr& A, Analysis& an, cudaStream_t st) {
+    const Schedule& up = an.blk_up;
+    const int64_t nb = up.nblocks;
+    an.mv_order.alloc(std::max<int64_t>(nb, 1));
+    if (nb == 0) return;
+    DevBuf<int32_t> key(nb), skey(nb), val(nb);
+    mv_keys<<<grid_for(nb, 256), 256, 0, st>>>(nb, an.bs, up.level.p, A.rp.p, A.cols.p, key.p, val.p);
+    CK_LAUNCH();
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, val.p, an.mv_order.p, static_cast<int>(nb), 0, 32,
+                                    st);
+    DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+    cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, val.p, an.mv_order.p, static_cast<int>(nb), 0, 32, st);
+    CK(cudaStreamSynchronize(st));
+}
+
 Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     if (m.an) return *m.an;
     const DevCsr& a = m.a;
@@ -630,6 +692,29 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     // (row-granular level sets are computed on request only: pclab_precond_levels)
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
     build_schedule(U, L, bs, true, lanes, an->blk_up, st);
+    if (an->bsr) {
+        for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
+            const DevCsr& M = sc == &an->blk_lo ? L : U;
+            const int64_t ns = sc->nitems * sc->per_item;
+            sc->slot_rp.alloc(std::max<int64_t>(ns * (bs + 1), 1));
+            if (ns > 0) {
+                slot_rp_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, bs, sc->slots.p, M.rp.p, sc->slot_rp.p);
+                CK_LAUNCH();
+            }
+        }
+    }
+    // upper sweep fused with the next iteration's A z (node-blocked A)
+    an->fused_up = false;
+    if (an->bsr && !(getenv("PCLAB_FUSE") && atoi(getenv("PCLAB_FUSE")) == 0)) {
+        DevBuf<int> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        bsr_check_full<<<grid_for(n / bs, 256), 256, 0, st>>>(n / bs, bs, a.rp.p, a.cols.p, bad.p);
+        CK_LAUNCH();
+        if (dev_read(bad.p, st) == 0) {
+            build_mv_order(a, *an, st);
+            an->fused_up = true;
+        }
+    }
     // chunked / TMA-fed sweeps (experimental, PCLAB_SWEEP=1|2): their
     // schedules and packed streams are only built when selected
     if (getenv("PCLAB_SWEEP") && atoi(getenv("PCLAB_SWEEP")) != 0) {

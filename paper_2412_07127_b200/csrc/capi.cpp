@@ -687,12 +687,12 @@ void pclab_set_stream(void* stream) {
 long long pclab_launch_count(void) { return launch_count(); }
 
 pclab_status pclab_pcg_profile(pclab_matrix* a, const pclab_precond* p, const double* b, double* x,
-                               int64_t max_iters, double* ms6) {
-    if (a == nullptr || p == nullptr || b == nullptr || x == nullptr || ms6 == nullptr)
+                               int64_t max_iters, double* ms8) {
+    if (a == nullptr || p == nullptr || b == nullptr || x == nullptr || ms8 == nullptr)
         return fail(PCLAB_ERR_ARGUMENT, "pclab_pcg_profile: null argument");
     return guarded([&] {
         if (p->p->a != a->m.get()) throw DimensionError("preconditioner built for another matrix");
-        pcg_solve(*a->m, *p->p, b, x, 1e-300, max_iters, false, lib_stream(), ms6);
+        pcg_solve(*a->m, *p->p, b, x, 1e-300, max_iters, false, lib_stream(), ms8);
     });
 }
 

@@ -82,6 +82,7 @@ struct Schedule {
     DevBuf<int64_t> item_first;  // [nitems] first position in `order`
     DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item
     DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
+    DevBuf<int64_t> slot_rp;     // [nitems * per_item * (bs + 1)] row pointers of the slot's block (bsr)
     int64_t max_level_width = 0;
     // chunked variant: contiguous chunks of `chunk_blocks` blocks, one CTA
     // each; inside a chunk, items of one local level (internal deps only)
@@ -107,6 +108,10 @@ struct Analysis {
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)
+    // backward sweep fused with w = A z (node-blocked A): the A block rows
+    // in the order their z inputs complete (max upper level over the row)
+    bool fused_up = false;
+    DevBuf<int32_t> mv_order;
     double ms = 0.0;         // wall time of the analysis (CUDA events)
 };
 
@@ -185,6 +190,10 @@ void trsv(const Analysis& an, const double* vals, const double* invd, const unsi
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, const unsigned char* pack,
                  bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
                  cudaStream_t st);
+// Backward sweep z = U^-1 y fused with w = A z (Analysis::fused_up).
+void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
+                       const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
+                       cudaStream_t st);
 void pack_factor(const Analysis& an, const double* lvals, const double* uvals, const double* invd,
                  DevBuf<unsigned char>& plo, DevBuf<unsigned char>& pup, cudaStream_t st);
 void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);

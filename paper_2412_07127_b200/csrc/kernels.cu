@@ -124,13 +124,41 @@ static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals
                                                           g_trace);
 }
 
+// CTAs of `kernel` (256 threads) the whole GPU holds at once.
+template <typename K>
+static unsigned resident_ctas(K kernel) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+    return static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+}
+
+// Round-robin items need every warp resident: the grid is capped at what
+// the GPU holds (measured best on configs[2]: as many warps as fit).
 template <int LG, int BS, bool UP>
 static void launch_bsr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                         cudaStream_t st) {
-    bsr_trsv_kernel<LG, BS, UP><<<trsv_grid(s, 2.0), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
-                                                              vals, invd, b, x, reset, done, ctr, trsv_tune(),
-                                                              g_trace);
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
+    static const unsigned cap = resident_ctas(bsr_trsv_kernel<LG, BS, UP>);
+    const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
+    bsr_trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, M.cols.p, vals, invd, b, x,
+                                                      reset, done, trsv_tune(), g_trace);
+}
+
+// CTAs given to the fused product (PCLAB_MV_CTAS overrides; default two per SM)
+static unsigned mv_ctas() {
+    static const int v = getenv("PCLAB_MV_CTAS") ? atoi(getenv("PCLAB_MV_CTAS")) : 0;
+    return static_cast<unsigned>(v > 0 ? v : 2 * sm_count());
+}
+
+template <int LG, int BS>
+static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
+                           const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
+                           cudaStream_t st) {
+    const Schedule& s = an.blk_up;
+    static const unsigned cap = resident_ctas(bsr_upper_mv_kernel<LG, BS>);
+    const unsigned nsweep = std::min(trsv_grid(s, 2.0), cap);
+    bsr_upper_mv_kernel<LG, BS><<<nsweep + mv_ctas(), 256, 0, st>>>(
+        s.nitems, s.slots.p, s.slot_rp.p, an.upper.cols.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
+        an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
 }
 
 // PCLAB_SWEEP=0 selects the warp-item sweep (global level order), default
@@ -212,10 +240,10 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool bsr, const d
         if (bsr) {
             switch (s.lanes) {
             case 2:
-            case 4: launch_bsr_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            case 8: launch_bsr_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            case 16: launch_bsr_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            default: launch_bsr_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
+            case 4: launch_bsr_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
+            default: launch_bsr_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
             }
             return;
         }
@@ -245,6 +273,31 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, con
         if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
         else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
         else launch_trsv_bs<1, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+    }
+    CK_LAUNCH();
+}
+
+// ctr[0..2] must be zero on entry (sweep items, CTA roles, product pairs).
+void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
+                       const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
+                       cudaStream_t st) {
+    if (an.blk_up.nitems == 0) return;
+    if (an.bs == 3) {
+        switch (an.blk_up.lanes) {
+            case 2:
+            case 4: launch_fused_t<4, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            case 8: launch_fused_t<8, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            case 16: launch_fused_t<16, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            default: launch_fused_t<32, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+        }
+    } else {
+        switch (an.blk_up.lanes) {
+            case 2:
+            case 4: launch_fused_t<4, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            case 8: launch_fused_t<8, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            case 16: launch_fused_t<16, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+            default: launch_fused_t<32, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
+        }
     }
     CK_LAUNCH();
 }

@@ -32,7 +32,7 @@ struct Scal {
     long long iter, max_iters;
     int done, converged, error, pad;
     unsigned ticket[4];
-    unsigned ctr[2];
+    unsigned ctr[4];  // sweep L items, sweep U items, fused CTA roles, product pairs
 };
 
 // Last-CTA finalisation of a per-CTA partial: returns true in the CTA
@@ -119,6 +119,41 @@ k_spmv_pap(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict_
         }
         S->ctr[0] = 0;
         S->ctr[1] = 0;
+        S->ctr[2] = 0;
+        S->ctr[3] = 0;
+    }
+}
+
+// Fused-product variant (Analysis::fused_up): w = A z came out of the
+// backward sweep, so p <- z + beta p, q <- w + beta q (= A p by linearity)
+// and pq in one vector pass; alpha = rz / pq.
+__global__ void __launch_bounds__(kT)
+k_pq(int64_t n, const double* __restrict__ z, const double* __restrict__ w, double* __restrict__ p,
+     double* __restrict__ q, Scal* S, double* part) {
+    if (S->done) return;
+    const double beta = S->beta;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        const double pi = fma(beta, p[i], z[i]);
+        const double qi = fma(beta, q[i], w[i]);
+        p[i] = pi;
+        q[i] = qi;
+        loc = fma(pi, qi, loc);
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
+        S->pap = tot;
+        if (!(tot > 0.0)) {
+            S->error = 1;
+            S->done = 1;
+        } else {
+            S->alpha = S->rz / tot;
+        }
+        S->ctr[0] = 0;
+        S->ctr[1] = 0;
+        S->ctr[2] = 0;
+        S->ctr[3] = 0;
     }
 }
 
@@ -337,7 +372,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     const int parts_max = sm_count() * 8;
     DevBuf<Scal> S(1);
-    DevBuf<double> part(parts_max), r(n), q(n), pa(n), pb(n), y, zbuf, tmp(n);
+    DevBuf<double> part(parts_max), r(n), q(n), pa(n), y, zbuf, wbuf, tmp(n);
     DevBuf<double> hist;
     if (record) hist.alloc(max_iters + 1);
     Scal h{};
@@ -373,6 +408,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         return rep;
     }
     const Analysis* an = factor ? a.an.get() : nullptr;
+    // backward sweep fused with the product (node-blocked matrices)
+    const bool fused = an && an->fused_up;
+    if (fused) wbuf.alloc(n);
     double* z = r.p;  // kind none: z aliases r
     if (factor) {
         y.alloc(n);
@@ -388,9 +426,12 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     {
         Timer tt(st);
         if (factor) {
-            CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 2, st));
+            CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
             launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
-            launch_trsv(*an, pc.uvals.p, pc.invd.p, pc.pack_up.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
+            if (fused)
+                launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, nullptr, S.p->ctr + 1, st);
+            else
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, pc.pack_up.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
@@ -399,11 +440,26 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     }
     k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
     CK(cudaMemsetAsync(pa.p, 0, sizeof(double) * n, st));
+    CK(cudaMemsetAsync(q.p, 0, sizeof(double) * n, st));  // fused: q <- w + 0 q
     CK_LAUNCH();
     // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
     // `mark` runs after each of the five kernels (event hook for profiling)
     auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
+        if (fused) {
+            // [p, q, alpha] -> [x, r] -> y = L^-1 r -> [z = U^-1 y, w = A z] -> beta
+            k_pq<<<vgrid, kT, 0, st>>>(n, z, wbuf.p, pp, q.p, S.p, part.p);
+            mark();
+            k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+            mark();
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            mark();
+            launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, &S.p->done, S.p->ctr + 1, st);
+            mark();
+            k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+            mark();
+            return;
+        }
         k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
         switch (lpr) {
             case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
@@ -437,14 +493,15 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK(cudaMallocHost(&hdone, sizeof(int)));
     if (prof_ms) {
         // eager iterations with an event between kernels: per-kernel device
-        // times [spmv_p, axpy, sweep L, sweep U, dot] averaged over iterations
+        // times averaged over iterations, [spmv_p, axpy, sweep L, sweep U,
+        // dot] or, fused, [pq, axpy, sweep L, sweep U + A z, dot]
         constexpr int kK = 5;
         cudaEvent_t ev[kK + 1];
         for (auto& e : ev) CK(cudaEventCreate(&e));
         double acc[kK] = {0, 0, 0, 0, 0};
         int done_iters = 0;
         double* pold = pa.p;
-        double* pnew = pb.p;
+        double* pnew = nullptr;
         for (;;) {
             int k = 0;
             CK(cudaEventRecord(ev[k++], st));
@@ -461,6 +518,8 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         }
         for (int t = 0; t < kK; ++t) prof_ms[t] = done_iters ? acc[t] / done_iters : 0.0;
         prof_ms[kK] = done_iters;
+        prof_ms[kK + 1] = fused ? 1.0 : 0.0;
+        prof_ms[kK + 2] = 0.0;
         for (auto& e : ev) cudaEventDestroy(e);
     } else {
         const int pairs = n > 2000000 ? 4 : 8;  // iterations per graph = 2 * pairs

@@ -8,6 +8,11 @@
 #ifndef TRSV_MINB
 #define TRSV_MINB 4
 #endif
+// the node-blocked sweep runs ~2 levels of items (<= 2 CTAs per SM): give
+// it the registers to keep the two items' operands without spilling
+#ifndef BSR_MINB
+#define BSR_MINB 2
+#endif
 
 namespace pclab_b200 {
 
@@ -283,6 +288,31 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
     }
 }
 
+// Per-item state of the node-blocked sweep.
+template <int BS>
+struct BsrMeta {
+    int64_t blk;  // -1: idle lane group
+    int64_t rp[BS + 1];
+    double rhs[BS];
+};
+
+// Slot and row pointers of item `it` (two independent loads: the schedule
+// stores each slot's row pointers, Schedule::slot_rp).
+template <int BS>
+__device__ __forceinline__ BsrMeta<BS> bsr_meta(int64_t it, int64_t nitems, int G, int grp,
+                                                const int32_t* __restrict__ slots,
+                                                const int64_t* __restrict__ srp) {
+    BsrMeta<BS> m;
+    const bool ok = it < nitems;
+    const int64_t k = it * G + grp;
+    m.blk = ok ? static_cast<int64_t>(__ldg(slots + k)) : -1;
+#pragma unroll
+    for (int t = 0; t <= BS; ++t) m.rp[t] = ok ? __ldg(srp + k * (BS + 1) + t) : 0;
+#pragma unroll
+    for (int t = 0; t < BS; ++t) m.rhs[t] = 0.0;
+    return m;
+}
+
 // Node-blocked sweep (Analysis::bsr: the off-block pattern is made of
 // whole BSxBS blocks shared by the block's BS rows -- elasticity, where the
 // dofs of a node couple to every dof of each neighbour node). Lane n of the
@@ -292,43 +322,42 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
 // predecessor poll followed by a second L2 round trip), and a neighbour's
 // values are read once instead of once per row.
 //
-// Measured on configs[2] (traces, tools/trace_trsv.py): deeper claim
-// pipelines (3 items per warp) and next-item operands held in registers
-// both start items earlier but lengthen every item's load chain, net
-// slower (1.50 / 1.92 ms vs 1.40 ms per sweep).
+// Items are dealt round-robin: warp w of W runs items w, w + W, w + 2W, ...
+// (all W warps resident). Every dependency of an item has a smaller index,
+// so the smallest unfinished item is always runnable: its warp has finished
+// everything before it. With the sequence known, nothing waits on a claim:
+// item k+2's slot and row pointers are loaded while item k runs, item k+1's
+// entries are pulled into L1 and its right-hand side into registers.
 template <int LG, int BS, bool UPPER>
-__global__ void __launch_bounds__(256, TRSV_MINB)
-bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __restrict__ crit,
-                const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
-                const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs,
-                double* out, double* reset, const int* __restrict__ done, unsigned* counter, int tune,
-                long long* trace) {
-    if (done && *done) return;
-    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+__device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ slots,
+                                          const int64_t* __restrict__ srp, const int32_t* __restrict__ cols,
+                                          const double* __restrict__ vals, const double* __restrict__ invd,
+                                          const double* rhs, double* out, double* reset, int64_t warp,
+                                          int64_t nwarps, unsigned sleep_ns, long long* trace) {
     constexpr int G = 32 / LG;
     constexpr int NIB = BS * (BS - 1) / 2;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
-    unsigned it = 0, next = 0;
-    if (lane == 0) {
-        it = atomicAdd(counter, 1u);
-        next = atomicAdd(counter, 1u);
+    int64_t it = warp;
+    BsrMeta<BS> m = bsr_meta<BS>(it, nitems, G, grp, slots, srp);
+    BsrMeta<BS> m1 = bsr_meta<BS>(it + nwarps, nitems, G, grp, slots, srp);
+    BsrMeta<BS> m2 = bsr_meta<BS>(it + 2 * nwarps, nitems, G, grp, slots, srp);
+    if (m.blk >= 0) {
+#pragma unroll
+        for (int t = 0; t < BS; ++t) m.rhs[t] = rhs[m.blk * BS + t];
     }
-    it = __shfl_sync(0xffffffffu, it, 0);
-    next = __shfl_sync(0xffffffffu, next, 0);
-    SweepMeta<BS> m = sweep_meta<BS>(it, nitems, G, grp, slots, crit, rp, rhs);
-    SweepMeta<BS> mn = sweep_meta<BS>(next, nitems, G, grp, slots, crit, rp, rhs);
     while (it < nitems) {
-        if (mn.blk >= 0) {
-            const int64_t e0 = mn.rp[0], e1 = mn.rp[BS];
+        if (m1.blk >= 0) {
+            // next item: its entries into L1, its right-hand side into registers
+            const int64_t e0 = m1.rp[0], e1 = m1.rp[BS];
             for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
             for (int64_t a = (e0 & ~31LL) + 32 * gl; a < e1; a += 32 * LG)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + a));
-            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + mn.blk * BS));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + m1.blk * BS));
+#pragma unroll
+            for (int t = 0; t < BS; ++t) m1.rhs[t] = rhs[m1.blk * BS + t];
         }
-        unsigned after = 0;
-        if (lane == 0) after = atomicAdd(counter, 1u);
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         const bool active = m.blk >= 0;
@@ -338,13 +367,10 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t
 #pragma unroll
         for (int t = 0; t < BS; ++t) ob[t] = UPPER ? m.rp[t] + (BS - t) : m.rp[t];
         const int nb = active ? static_cast<int>((UPPER ? m.rp[1] - ob[0] : m.rp[1] - 1 - m.rp[0]) / BS) : 0;
-        double brhs[BS], binv[BS], bin[NIB > 0 ? NIB : 1];
+        double binv[BS], bin[NIB > 0 ? NIB : 1];
         if (active && gl == 0) {
 #pragma unroll
-            for (int t = 0; t < BS; ++t) {
-                brhs[t] = m.rhs[t];
-                binv[t] = __ldg(invd + r0 + t);
-            }
+            for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
             int q = 0;
 #pragma unroll
             for (int t = 0; t < BS; ++t)
@@ -401,7 +427,6 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t
         }
         long long trg = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
-        after = __shfl_sync(0xffffffffu, after, 0);
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
         if (active && gl == 0) {
@@ -410,7 +435,7 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t
                 int q = 0;
 #pragma unroll
                 for (int t = 0; t < BS; ++t) {
-                    double s = brhs[t] - acc[t];
+                    double s = m.rhs[t] - acc[t];
 #pragma unroll
                     for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
                     xb[t] = s * binv[t];
@@ -418,7 +443,7 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t
             } else {
 #pragma unroll
                 for (int t = BS - 1; t >= 0; --t) {
-                    double s = brhs[t] - acc[t];
+                    double s = m.rhs[t] - acc[t];
                     int q = 0;
 #pragma unroll
                     for (int r = 0; r < t; ++r) q += BS - 1 - r;
@@ -440,11 +465,164 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t
         }
         __syncwarp();
         if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
-        it = next;
-        m = mn;
-        next = after;
-        mn = sweep_meta<BS>(after, nitems, G, grp, slots, crit, rp, rhs);
+        it += nwarps;
+        m = m1;
+        m1 = m2;
+        m2 = bsr_meta<BS>(it + 2 * nwarps, nitems, G, grp, slots, srp);
     }
+}
+
+template <int LG, int BS, bool UPPER>
+__global__ void __launch_bounds__(256, BSR_MINB)
+bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+                const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                const double* __restrict__ invd, const double* rhs, double* out, double* reset,
+                const int* __restrict__ done, int tune, long long* trace) {
+    if (done && *done) return;
+    bsr_sweep<LG, BS, UPPER>(nitems, slots, srp, cols, vals, invd, rhs, out, reset,
+                             (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                             (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, static_cast<unsigned>(tune >> 8),
+                             trace);
+}
+
+// w = A z for node-blocked A, following the backward sweep's frontier: a
+// warp takes two block rows (in the order their z inputs complete,
+// Analysis::mv_order), lane n owns neighbour block n of both, polls its z
+// values like a sweep item and the warp writes the 2 x BS products. The
+// next pair's row pointers are loaded one pair ahead.
+template <int BS>
+struct MvMeta {
+    int64_t blk[2];
+    int64_t rp[2][BS + 1];
+};
+
+template <int BS>
+__device__ __forceinline__ MvMeta<BS> mv_meta(unsigned c, int64_t nb, const int32_t* __restrict__ order,
+                                              const int64_t* __restrict__ arp) {
+    MvMeta<BS> m;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int64_t k = 2 * static_cast<int64_t>(c) + j;
+        m.blk[j] = k < nb ? static_cast<int64_t>(__ldg(order + k)) : -1;
+#pragma unroll
+        for (int t = 0; t <= BS; ++t) m.rp[j][t] = m.blk[j] >= 0 ? __ldg(arp + m.blk[j] * BS + t) : 0;
+    }
+    return m;
+}
+
+template <int BS>
+__device__ __forceinline__ void bsr_mv(int64_t nb, const int32_t* __restrict__ order,
+                                       const int64_t* __restrict__ arp, const int32_t* __restrict__ acols,
+                                       const double* __restrict__ avals, const double* z, double* __restrict__ w,
+                                       unsigned* counter) {
+    const int lane = threadIdx.x & 31;
+    const int64_t npairs = (nb + 1) / 2;
+    unsigned c = 0, cn = 0;
+    if (lane == 0) {
+        c = atomicAdd(counter, 1u);
+        cn = atomicAdd(counter, 1u);
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    cn = __shfl_sync(0xffffffffu, cn, 0);
+    MvMeta<BS> m = mv_meta<BS>(c, nb, order, arp);
+    MvMeta<BS> mn = mv_meta<BS>(cn, nb, order, arp);
+    while (c < npairs) {
+        unsigned after = 0;
+        if (lane == 0) after = atomicAdd(counter, 1u);
+        int nbk[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) nbk[j] = m.blk[j] >= 0 ? static_cast<int>((m.rp[j][1] - m.rp[j][0]) / BS) : 0;
+        const int nbmax = max(nbk[0], nbk[1]);
+        double acc[2][BS];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int t = 0; t < BS; ++t) acc[j][t] = 0.0;
+        for (int n0 = 0; n0 < nbmax; n0 += 32) {
+            const int n = n0 + lane;
+            double a[2][BS][BS], xv[2][BS];
+            int32_t xc[2];
+            bool own[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                own[j] = n < nbk[j];
+                xc[j] = own[j] ? ld_stream(acols + m.rp[j][0] + BS * n) : 0;
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc)
+                        a[j][t][cc] = own[j] ? ld_stream(avals + m.rp[j][t] + BS * n + cc) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc) xv[j][cc] = own[j] ? ld_relaxed(z + xc[j] + cc) : 0.0;
+            bool pend = false;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc) pend |= own[j] && is_pending(xv[j][cc]);
+            while (__any_sync(0xffffffffu, pend)) {
+                pend = false;
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc)
+                        if (own[j] && is_pending(xv[j][cc])) {
+                            xv[j][cc] = ld_relaxed(z + xc[j] + cc);
+                            pend |= is_pending(xv[j][cc]);
+                        }
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) acc[j][t] = fma(a[j][t][cc], xv[j][cc], acc[j][t]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int t = 0; t < BS; ++t) acc[j][t] = group_sum<32>(acc[j][t]);
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                if (m.blk[j] >= 0)
+#pragma unroll
+                    for (int t = 0; t < BS; ++t) w[m.blk[j] * BS + t] = acc[j][t];
+        }
+        after = __shfl_sync(0xffffffffu, after, 0);
+        c = cn;
+        m = mn;
+        cn = after;
+        mn = mv_meta<BS>(after, nb, order, arp);
+    }
+}
+
+// Backward sweep z = U^-1 y and w = A z in one launch. The first `nsweep`
+// CTAs to start (ticket counter[1]) run the sweep (nsweep must fit on the
+// GPU at once); the rest run the product on counter[2]. Product warps only
+// wait on sweep items, and the sweep CTAs are the first ones resident.
+template <int LG, int BS>
+__global__ void __launch_bounds__(256, BSR_MINB)
+bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+                    const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                    const double* __restrict__ invd, const double* rhs, double* out, double* reset,
+                    unsigned nsweep, int64_t nb, const int32_t* __restrict__ order,
+                    const int64_t* __restrict__ arp, const int32_t* __restrict__ acols,
+                    const double* __restrict__ avals, double* __restrict__ w, const int* __restrict__ done,
+                    unsigned* counters, int tune, long long* trace) {
+    if (done && *done) return;
+    __shared__ unsigned role;
+    if (threadIdx.x == 0) role = atomicAdd(counters + 1, 1u);
+    __syncthreads();
+    if (role < nsweep)
+        bsr_sweep<LG, BS, true>(nitems, slots, srp, cols, vals, invd, rhs, out, reset,
+                                static_cast<int64_t>(role) * (blockDim.x >> 5) + (threadIdx.x >> 5),
+                                static_cast<int64_t>(nsweep) * (blockDim.x >> 5), static_cast<unsigned>(tune >> 8),
+                                trace);
+    else
+        bsr_mv<BS>(nb, order, arp, acols, avals, out, w, counters + 2);
 }
 
 // ------------------------------------------------------------------------
