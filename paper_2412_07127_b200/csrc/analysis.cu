@@ -297,13 +297,47 @@ __global__ void slots_fill(int64_t nitems, int per_item, const int32_t* __restri
 }
 
 // Row pointers of every slot's block, stored with the schedule so an
-// item's first dependent load is its entries (node-blocked sweep).
+// item's first dependent load is its entries (node-blocked sweep): record
+// k = {rp[first row], row lengths packed 16 bits per row}.
 __global__ void slot_rp_fill(int64_t nslots, int bs, const int32_t* __restrict__ slots,
-                             const int64_t* __restrict__ rp, int64_t* __restrict__ srp) {
+                             const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+                             int64_t* __restrict__ srp, int* __restrict__ bad) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (k >= nslots) return;
     const int32_t b = slots[k];
-    for (int t = 0; t <= bs; ++t) srp[k * (bs + 1) + t] = b >= 0 ? rp[static_cast<int64_t>(b) * bs + t] : 0;
+    int64_t r0 = 0;
+    unsigned long long lens = 0;
+    if (b >= 0) {
+        const int64_t i = static_cast<int64_t>(b) * bs;
+        r0 = rp[i];
+        for (int t = 0; t < bs; ++t) {
+            const int64_t len = rp[i + t + 1] - rp[i + t];
+            if (len > 0xffff) *bad = 1;
+            lens |= static_cast<unsigned long long>(len & 0xffff) << (16 * t);
+        }
+    }
+    srp[4 * k] = r0;
+    srp[4 * k + 1] = static_cast<int64_t>(lens);
+    srp[4 * k + 2] = b >= 0 ? bp[b] : 0;
+    srp[4 * k + 3] = 0;
+}
+
+// Block-column view (BlockCols). mode 0: L (off-block entries first),
+// 1: U (bs in-block entries first in the block's first row), 2: A (all).
+__global__ void bc_count(int64_t nb, int bs, int mode, const int64_t* __restrict__ rp, int64_t* __restrict__ cnt) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t len = rp[b * bs + 1] - rp[b * bs];
+    cnt[b] = (len - (mode == 0 ? 1 : mode == 1 ? bs : 0)) / bs;
+}
+
+__global__ void bc_fill(int64_t nb, int bs, int mode, const int64_t* __restrict__ rp,
+                        const int32_t* __restrict__ cols, const int64_t* __restrict__ bp,
+                        int32_t* __restrict__ bcol) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t first = rp[b * bs] + (mode == 1 ? bs : 0);
+    for (int64_t k = bp[b]; k < bp[b + 1]; ++k) bcol[k] = cols[first + (k - bp[b]) * bs];
 }
 
 __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* __restrict__ start,
@@ -600,6 +634,23 @@ static void build_chunk_schedule(const DevCsr& pred, int bs, bool upper, int64_t
     }
 }
 
+static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, cudaStream_t st) {
+    const int64_t nb = M.n / bs;
+    bc.bp.alloc(nb + 1);
+    if (nb > 0) {
+        bc_count<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, mode, M.rp.p, bc.bp.p);
+        CK_LAUNCH();
+    }
+    CK(cudaMemsetAsync(bc.bp.p + nb, 0, sizeof(int64_t), st));
+    scan_inplace(bc.bp.p, nb + 1, st);
+    const int64_t tot = dev_read(bc.bp.p + nb, st);
+    bc.bcol.alloc(std::max<int64_t>(tot, 1));
+    if (nb > 0) {
+        bc_fill<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, mode, M.rp.p, M.cols.p, bc.bp.p, bc.bcol.p);
+        CK_LAUNCH();
+    }
+}
+
 // A block rows sorted by the backward-sweep level that completes their z
 // inputs (Analysis::mv_order).
 static void build_mv_order(const DevCsr& A, Analysis& an, cudaStream_t st) {
@@ -693,29 +744,42 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
     build_schedule(U, L, bs, true, lanes, an->blk_up, st);
     if (an->bsr) {
+        build_block_cols(L, bs, 0, an->lbc, st);
+        build_block_cols(U, bs, 1, an->ubc, st);
+        DevBuf<int> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
         for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
-            const DevCsr& M = sc == &an->blk_lo ? L : U;
+            const bool lo = sc == &an->blk_lo;
+            const DevCsr& M = lo ? L : U;
             const int64_t ns = sc->nitems * sc->per_item;
-            sc->slot_rp.alloc(std::max<int64_t>(ns * (bs + 1), 1));
+            sc->slot_rp.alloc(std::max<int64_t>(4 * ns, 1));
             if (ns > 0) {
-                slot_rp_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, bs, sc->slots.p, M.rp.p, sc->slot_rp.p);
+                slot_rp_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, bs, sc->slots.p, M.rp.p,
+                                                                (lo ? an->lbc : an->ubc).bp.p, sc->slot_rp.p, bad.p);
                 CK_LAUNCH();
             }
+        }
+        if (dev_read(bad.p, st) != 0) an->bsr = false;  // a row too long for the packed record
+    }
+    // node-blocked A: the PCG product reads one column index per block
+    an->a_bsr = false;
+    if (an->bsr) {
+        DevBuf<int> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        bsr_check_full<<<grid_for(n / bs, 256), 256, 0, st>>>(n / bs, bs, a.rp.p, a.cols.p, bad.p);
+        CK_LAUNCH();
+        if (dev_read(bad.p, st) == 0) {
+            build_block_cols(a, bs, 2, an->abc, st);
+            an->a_bsr = true;
         }
     }
     // upper sweep fused with the next iteration's A z (node-blocked A).
     // Opt-in (PCLAB_FUSE=1): on configs[2] the product CTAs slow the sweep
     // more than the separate SpMV costs (2.37 vs 1.02 + 1.04 ms)
     an->fused_up = false;
-    if (an->bsr && getenv("PCLAB_FUSE") && atoi(getenv("PCLAB_FUSE")) != 0) {
-        DevBuf<int> bad(1);
-        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-        bsr_check_full<<<grid_for(n / bs, 256), 256, 0, st>>>(n / bs, bs, a.rp.p, a.cols.p, bad.p);
-        CK_LAUNCH();
-        if (dev_read(bad.p, st) == 0) {
-            build_mv_order(a, *an, st);
-            an->fused_up = true;
-        }
+    if (an->a_bsr && getenv("PCLAB_FUSE") && atoi(getenv("PCLAB_FUSE")) != 0) {
+        build_mv_order(a, *an, st);
+        an->fused_up = true;
     }
     // chunked / TMA-fed sweeps (experimental, PCLAB_SWEEP=1|2): their
     // schedules and packed streams are only built when selected

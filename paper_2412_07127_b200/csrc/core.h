@@ -82,7 +82,8 @@ struct Schedule {
     DevBuf<int64_t> item_first;  // [nitems] first position in `order`
     DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item
     DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
-    DevBuf<int64_t> slot_rp;     // [nitems * per_item * (bs + 1)] row pointers of the slot's block (bsr)
+    DevBuf<int64_t> slot_rp;     // [nitems * per_item * 4] {first row pointer, packed row lengths,
+                                 //  block-column offset, 0} of the slot's block (bsr)
     int64_t max_level_width = 0;
     // chunked variant: contiguous chunks of `chunk_blocks` blocks, one CTA
     // each; inside a chunk, items of one local level (internal deps only)
@@ -95,6 +96,16 @@ struct Schedule {
     int64_t pack_bytes = 0, pack_max_item = 0;
 };
 
+// Block-column view of a node-blocked CSR matrix (Analysis::bsr): block
+// row b's off-block neighbour blocks are bcol[bp[b] .. bp[b + 1]), each
+// stored as its first column (a multiple of bs). One index per bs x bs
+// block instead of one per entry: the sweeps and the product read a ninth
+// of the column indices.
+struct BlockCols {
+    DevBuf<int64_t> bp;    // [nblocks + 1]
+    DevBuf<int32_t> bcol;  // [bp[nblocks]]
+};
+
 // Symbolic analysis of a structurally symmetric matrix (the reference's
 // lower_triangle + csr_transpose, sparse.cpp:137/189, done once on the
 // device): L pattern with A's lower values, U = L^T pattern, the slot map
@@ -105,6 +116,9 @@ struct Analysis {
     DevBuf<int64_t> u2l;     // [nnz(U)] position in L of each U entry
     int bs = 1;              // detected dof block size (3 for elasticity)
     bool bsr = false;        // off-block pattern made of whole bs x bs blocks
+    BlockCols lbc, ubc;      // block columns of L / U (bsr)
+    bool a_bsr = false;      // A itself node-blocked: product through abc
+    BlockCols abc;
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)

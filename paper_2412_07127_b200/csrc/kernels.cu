@@ -35,6 +35,30 @@ spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict
     }
 }
 
+template <int BS, int R>
+__global__ void __launch_bounds__(256)
+spmv_bsr_kernel(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+                const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ x,
+                double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t b0 = gw * R; b0 < nb; b0 += nw * R) {
+        double acc[R][BS];
+        bsr_block_dots<BS, R>(b0, nb, rp, bp, bcol, vals, x, acc);
+        if (lane < R * BS) {
+            const int j = lane / BS, t = lane % BS;
+            double v = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < R; ++jj)
+#pragma unroll
+                for (int tt = 0; tt < BS; ++tt)
+                    if (jj == j && tt == t) v = acc[jj][tt];
+            if (b0 + j < nb) y[(b0 + j) * BS + t] = v;
+        }
+    }
+}
+
 __global__ void gather_kernel(int64_t m, const int64_t* __restrict__ idx, const double* __restrict__ src,
                               double* __restrict__ dst) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -74,6 +98,15 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
     const int64_t n = a.a.n;
     if (n == 0) return;
     const unsigned grid = static_cast<unsigned>(sm_count() * 8);
+    if (a.an && a.an->a_bsr) {  // node-blocked: one column index per block
+        const BlockCols& bc = a.an->abc;
+        if (a.an->bs == 3)
+            spmv_bsr_kernel<3, 2><<<grid, 256, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
+        else
+            spmv_bsr_kernel<2, 2><<<grid, 256, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
+        CK_LAUNCH();
+        return;
+    }
     switch (spmv_lanes(a)) {
         case 4:
         case 5: spmv_kernel<4><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
@@ -135,11 +168,11 @@ static unsigned resident_ctas(K kernel) {
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
 template <int LG, int BS, bool UP>
-static void launch_bsr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
+static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
                          const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
     static const unsigned cap = resident_ctas(bsr_trsv_kernel<LG, BS, UP>);
     const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
-    bsr_trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, M.cols.p, vals, invd, b, x,
+    bsr_trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, bcol, vals, invd, b, x,
                                                       reset, done, trsv_tune(), g_trace);
 }
 
@@ -157,7 +190,7 @@ static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uv
     static const unsigned cap = resident_ctas(bsr_upper_mv_kernel<LG, BS>);
     const unsigned nsweep = std::min(trsv_grid(s, 2.0), cap);
     bsr_upper_mv_kernel<LG, BS><<<nsweep + mv_ctas(), 256, 0, st>>>(
-        s.nitems, s.slots.p, s.slot_rp.p, an.upper.cols.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
+        s.nitems, s.slots.p, s.slot_rp.p, an.ubc.bcol.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
         an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
 }
 
@@ -213,7 +246,7 @@ static void launch_tma_t(const Schedule& s, const unsigned char* pack, const dou
 }
 
 template <int BS, bool UP>
-static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool bsr, const double* vals,
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const int32_t* bcol, const double* vals,
                            const double* invd, const unsigned char* pack, const double* b, double* x, double* reset,
                            const int* done, unsigned* ctr, cudaStream_t st) {
     if (sweep_mode() == 2 && pack && s.nchunks > 0 && s.pack_max_item <= kSlotBytes) {
@@ -237,13 +270,13 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool bsr, const d
         return;
     }
     if constexpr (BS > 1) {
-        if (bsr) {
+        if (bcol) {
             switch (s.lanes) {
             case 2:
-            case 4: launch_bsr_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
-            case 8: launch_bsr_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
-            case 16: launch_bsr_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
-            default: launch_bsr_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, st); break;
+            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
+            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
             }
             return;
         }
@@ -264,15 +297,16 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, con
                  cudaStream_t st) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
+    const int32_t* bcol = an.bsr ? (upper ? an.ubc : an.lbc).bcol.p : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, an.bsr, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
     }
     CK_LAUNCH();
 }

@@ -14,6 +14,7 @@
 // captured in a CUDA graph (every kernel no-ops once `done` is set) and the
 // host polls the flag once per graph launch; the iteration count is exact.
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
@@ -140,6 +141,50 @@ k_pq(int64_t n, const double* __restrict__ z, const double* __restrict__ w, doub
         p[i] = pi;
         q[i] = qi;
         loc = fma(pi, qi, loc);
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
+        S->pap = tot;
+        if (!(tot > 0.0)) {
+            S->error = 1;
+            S->done = 1;
+        } else {
+            S->alpha = S->rz / tot;
+        }
+        S->ctr[0] = 0;
+        S->ctr[1] = 0;
+        S->ctr[2] = 0;
+        S->ctr[3] = 0;
+    }
+}
+
+// q = A p and pAp for a node-blocked A (Analysis::a_bsr): one warp per R
+// block rows, one column index per BSxBS block.
+template <int BS, int R>
+__global__ void __launch_bounds__(kT)
+k_spmv_bsr_pap(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+               const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p,
+               double* __restrict__ q, Scal* S, double* part) {
+    if (S->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * kT) >> 5;
+    double loc = 0.0;
+    for (int64_t b0 = gw * R; b0 < nb; b0 += nw * R) {
+        double acc[R][BS];
+        bsr_block_dots<BS, R>(b0, nb, rp, bp, bcol, vals, p, acc);
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (b0 + j >= nb) break;
+#pragma unroll
+                for (int t = 0; t < BS; ++t) {
+                    const int64_t row = (b0 + j) * BS + t;
+                    q[row] = acc[j][t];
+                    loc = fma(p[row], acc[j][t], loc);
+                }
+            }
+        }
     }
     double tot;
     if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
@@ -461,7 +506,15 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             return;
         }
         k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
-        switch (lpr) {
+        if (an && an->a_bsr) {
+            const BlockCols& bc = an->abc;
+            if (an->bs == 3)
+                k_spmv_bsr_pap<3, 2><<<sgrid, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
+                                                          S.p, part.p);
+            else
+                k_spmv_bsr_pap<2, 2><<<sgrid, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
+                                                          S.p, part.p);
+        } else switch (lpr) {
             case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 9: k_spmv_pap<8, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
@@ -521,8 +574,17 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         prof_ms[kK + 1] = fused ? 1.0 : 0.0;
         prof_ms[kK + 2] = 0.0;
         for (auto& e : ev) cudaEventDestroy(e);
+    } else if (getenv("PCLAB_PCG_GRAPH") && atoi(getenv("PCLAB_PCG_GRAPH")) == 0) {
+        // developer knob: stream-launched iterations, done flag read every 8
+        for (;;) {
+            for (int k = 0; k < 8; ++k) iteration(pa.p, nullptr);
+            CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (*hdone) break;
+        }
     } else {
-        const int pairs = n > 2000000 ? 4 : 8;  // iterations per graph = 2 * pairs
+        static const int pairs_env = getenv("PCLAB_GRAPH_PAIRS") ? atoi(getenv("PCLAB_GRAPH_PAIRS")) : 0;
+        const int pairs = pairs_env > 0 ? pairs_env : (n > 2000000 ? 4 : 8);  // iterations per graph = 2 * pairs
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         const long long before = launch_count();
@@ -536,11 +598,16 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         size_t nodes = 0;
         CK(cudaGraphGetNodes(graph, nullptr, &nodes));
         g_launches = before;  // captured launches are counted per replay below
+        static const bool gtrace = getenv("PCLAB_PCG_TRACE") != nullptr;
         for (;;) {
+            const auto t0 = std::chrono::steady_clock::now();
             CK(cudaGraphLaunch(exec, st));
             count_launches(static_cast<long long>(nodes));
             CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+            if (gtrace)
+                fprintf(stderr, "graph %.3f ms\n",
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
             if (*hdone) break;
         }
         cudaGraphExecDestroy(exec);

@@ -45,6 +45,61 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp,
     return group_sum<LPR>(acc);
 }
 
+// R consecutive block rows b0.. of a node-blocked matrix times x, one warp:
+// lane n owns neighbour block n of every row (32-wide rounds), all index
+// and value loads of the R rows are issued before the first x gather.
+// acc[j][t] = (A x)_{(b0 + j) BS + t}, valid in every lane.
+template <int BS, int R>
+__device__ __forceinline__ void bsr_block_dots(int64_t b0, int64_t nb, const int64_t* __restrict__ rp,
+                                               const int64_t* __restrict__ bp, const int32_t* __restrict__ bcol,
+                                               const double* __restrict__ vals, const double* __restrict__ x,
+                                               double (&acc)[R][BS]) {
+    const int lane = threadIdx.x & 31;
+    int64_t r[R][BS], c0[R];
+    int cnt[R];
+    int cmax = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const bool ok = b0 + j < nb;
+#pragma unroll
+        for (int t = 0; t < BS; ++t) r[j][t] = ok ? __ldg(rp + (b0 + j) * BS + t) : 0;
+        c0[j] = ok ? __ldg(bp + b0 + j) : 0;
+        cnt[j] = ok ? static_cast<int>(__ldg(bp + b0 + j + 1) - c0[j]) : 0;
+        cmax = max(cmax, cnt[j]);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[j][t] = 0.0;
+    }
+    for (int n0 = 0; n0 < cmax; n0 += 32) {
+        const int n = n0 + lane;
+        double a[R][BS][BS];
+        int32_t xc[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const bool own = n < cnt[j];
+            xc[j] = own ? __ldg(bcol + c0[j] + n) : -1;
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) a[j][t][c] = own ? __ldg(vals + r[j][t] + BS * n + c) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            if (xc[j] < 0) continue;
+            double xv[BS];
+#pragma unroll
+            for (int c = 0; c < BS; ++c) xv[c] = __ldg(x + xc[j] + c);
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[j][t] = fma(a[j][t][c], xv[c], acc[j][t]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[j][t] = group_sum<32>(acc[j][t]);
+}
+
 // Per-item state of a sweep, loaded one item ahead.
 template <int BS>
 struct SweepMeta {
@@ -288,29 +343,34 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
     }
 }
 
-// Per-item state of the node-blocked sweep.
-template <int BS>
-struct BsrMeta {
-    int64_t blk;  // -1: idle lane group
-    int64_t rp[BS + 1];
-    double rhs[BS];
+// Per-item state of the node-blocked sweep: the slot's block, its first
+// row pointer and packed row lengths (Schedule::slot_rp), and -- for the
+// next two items -- the right-hand side.
+struct BsrSlot {
+    int32_t blk;  // -1: idle lane group
+    int64_t r0;
+    unsigned long long lens;
+    int64_t bp;   // first block column of the block row
 };
 
-// Slot and row pointers of item `it` (two independent loads: the schedule
-// stores each slot's row pointers, Schedule::slot_rp).
-template <int BS>
-__device__ __forceinline__ BsrMeta<BS> bsr_meta(int64_t it, int64_t nitems, int G, int grp,
-                                                const int32_t* __restrict__ slots,
-                                                const int64_t* __restrict__ srp) {
-    BsrMeta<BS> m;
+__device__ __forceinline__ BsrSlot bsr_slot(int64_t it, int64_t nitems, int G, int grp,
+                                            const int32_t* __restrict__ slots, const int64_t* __restrict__ srp) {
+    BsrSlot m;
     const bool ok = it < nitems;
     const int64_t k = it * G + grp;
-    m.blk = ok ? static_cast<int64_t>(__ldg(slots + k)) : -1;
-#pragma unroll
-    for (int t = 0; t <= BS; ++t) m.rp[t] = ok ? __ldg(srp + k * (BS + 1) + t) : 0;
-#pragma unroll
-    for (int t = 0; t < BS; ++t) m.rhs[t] = 0.0;
+    m.blk = ok ? __ldg(slots + k) : -1;
+    const longlong2 v = ok ? __ldg(reinterpret_cast<const longlong2*>(srp) + 2 * k) : make_longlong2(0, 0);
+    m.r0 = v.x;
+    m.lens = static_cast<unsigned long long>(v.y);
+    m.bp = ok ? __ldg(srp + 4 * k + 2) : 0;
     return m;
+}
+
+template <int BS>
+__device__ __forceinline__ void slot_rows(const BsrSlot& m, int64_t (&rp)[BS + 1]) {
+    rp[0] = m.r0;
+#pragma unroll
+    for (int t = 0; t < BS; ++t) rp[t + 1] = rp[t] + static_cast<int64_t>((m.lens >> (16 * t)) & 0xffff);
 }
 
 // Node-blocked sweep (Analysis::bsr: the off-block pattern is made of
@@ -325,12 +385,13 @@ __device__ __forceinline__ BsrMeta<BS> bsr_meta(int64_t it, int64_t nitems, int 
 // Items are dealt round-robin: warp w of W runs items w, w + W, w + 2W, ...
 // (all W warps resident). Every dependency of an item has a smaller index,
 // so the smallest unfinished item is always runnable: its warp has finished
-// everything before it. With the sequence known, nothing waits on a claim:
-// item k+2's slot and row pointers are loaded while item k runs, item k+1's
-// entries are pulled into L1 and its right-hand side into registers.
+// everything before it. With the sequence known, nothing waits on a claim
+// and every load is issued a whole item before its value is needed:
+//   item k+3: slot record        item k+2: entries prefetched into L1
+//   item k+1: right-hand side    item k:   entries, dependency polls
 template <int LG, int BS, bool UPPER>
 __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ slots,
-                                          const int64_t* __restrict__ srp, const int32_t* __restrict__ cols,
+                                          const int64_t* __restrict__ srp, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
                                           const double* rhs, double* out, double* reset, int64_t warp,
                                           int64_t nwarps, unsigned sleep_ns, long long* trace) {
@@ -339,34 +400,44 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     int64_t it = warp;
-    BsrMeta<BS> m = bsr_meta<BS>(it, nitems, G, grp, slots, srp);
-    BsrMeta<BS> m1 = bsr_meta<BS>(it + nwarps, nitems, G, grp, slots, srp);
-    BsrMeta<BS> m2 = bsr_meta<BS>(it + 2 * nwarps, nitems, G, grp, slots, srp);
-    if (m.blk >= 0) {
+    BsrSlot m = bsr_slot(it, nitems, G, grp, slots, srp);
+    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+    double rhs0[BS], rhs1[BS];
 #pragma unroll
-        for (int t = 0; t < BS; ++t) m.rhs[t] = rhs[m.blk * BS + t];
+    for (int t = 0; t < BS; ++t) {
+        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
+        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
     }
-    while (it < nitems) {
-        if (m1.blk >= 0) {
-            // next item: its entries into L1, its right-hand side into registers
-            const int64_t e0 = m1.rp[0], e1 = m1.rp[BS];
+    auto prefetch = [&](const BsrSlot& q) {
+        if (q.blk >= 0) {
+            int64_t rq[BS + 1];
+            slot_rows<BS>(q, rq);
+            const int64_t e0 = rq[0], e1 = rq[BS];
             for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
-            for (int64_t a = (e0 & ~31LL) + 32 * gl; a < e1; a += 32 * LG)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + a));
-            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + m1.blk * BS));
-#pragma unroll
-            for (int t = 0; t < BS; ++t) m1.rhs[t] = rhs[m1.blk * BS + t];
+            if (gl == 0) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(bcol + q.bp));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + static_cast<int64_t>(q.blk) * BS));
+            }
         }
+    };
+    prefetch(m);
+    prefetch(m1);
+    while (it < nitems) {
+        prefetch(m2);
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         const bool active = m.blk >= 0;
-        const int64_t r0 = active ? m.blk * BS : 0;
+        const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
+        int64_t mrp[BS + 1];
+        slot_rows<BS>(m, mrp);
         // off-block entries of row t start at ob[t]; nb neighbour blocks
         int64_t ob[BS];
 #pragma unroll
-        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? m.rp[t] + (BS - t) : m.rp[t];
-        const int nb = active ? static_cast<int>((UPPER ? m.rp[1] - ob[0] : m.rp[1] - 1 - m.rp[0]) / BS) : 0;
+        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
+        const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
         double binv[BS], bin[NIB > 0 ? NIB : 1];
         if (active && gl == 0) {
 #pragma unroll
@@ -376,8 +447,8 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             for (int t = 0; t < BS; ++t)
 #pragma unroll
                 for (int s = 0; s < BS; ++s) {
-                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + m.rp[t + 1] - (t + 1) + s);
-                    if (UPPER && s > t) bin[q++] = ld_stream(vals + m.rp[t] + (s - t));
+                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
+                    if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
                 }
         }
         double acc[BS];
@@ -391,7 +462,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             double a[BS][BS], xv[BS];
             int32_t xc = 0;
             if (own) {
-                xc = ld_stream(cols + ob[0] + BS * n);
+                xc = ld_stream(bcol + m.bp + n);
 #pragma unroll
                 for (int t = 0; t < BS; ++t)
 #pragma unroll
@@ -435,7 +506,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
                 int q = 0;
 #pragma unroll
                 for (int t = 0; t < BS; ++t) {
-                    double s = m.rhs[t] - acc[t];
+                    double s = rhs0[t] - acc[t];
 #pragma unroll
                     for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
                     xb[t] = s * binv[t];
@@ -443,7 +514,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             } else {
 #pragma unroll
                 for (int t = BS - 1; t >= 0; --t) {
-                    double s = m.rhs[t] - acc[t];
+                    double s = rhs0[t] - acc[t];
                     int q = 0;
 #pragma unroll
                     for (int r = 0; r < t; ++r) q += BS - 1 - r;
@@ -468,18 +539,24 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         it += nwarps;
         m = m1;
         m1 = m2;
-        m2 = bsr_meta<BS>(it + 2 * nwarps, nitems, G, grp, slots, srp);
+        m2 = m3;
+        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            rhs0[t] = rhs1[t];
+            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+        }
     }
 }
 
 template <int LG, int BS, bool UPPER>
 __global__ void __launch_bounds__(256, BSR_MINB)
 bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
-                const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                 const double* __restrict__ invd, const double* rhs, double* out, double* reset,
                 const int* __restrict__ done, int tune, long long* trace) {
     if (done && *done) return;
-    bsr_sweep<LG, BS, UPPER>(nitems, slots, srp, cols, vals, invd, rhs, out, reset,
+    bsr_sweep<LG, BS, UPPER>(nitems, slots, srp, bcol, vals, invd, rhs, out, reset,
                              (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
                              (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, static_cast<unsigned>(tune >> 8),
                              trace);
@@ -606,7 +683,7 @@ __device__ __forceinline__ void bsr_mv(int64_t nb, const int32_t* __restrict__ o
 template <int LG, int BS>
 __global__ void __launch_bounds__(256, BSR_MINB)
 bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
-                    const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                    const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                     const double* __restrict__ invd, const double* rhs, double* out, double* reset,
                     unsigned nsweep, int64_t nb, const int32_t* __restrict__ order,
                     const int64_t* __restrict__ arp, const int32_t* __restrict__ acols,
@@ -617,7 +694,7 @@ bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int
     if (threadIdx.x == 0) role = atomicAdd(counters + 1, 1u);
     __syncthreads();
     if (role < nsweep)
-        bsr_sweep<LG, BS, true>(nitems, slots, srp, cols, vals, invd, rhs, out, reset,
+        bsr_sweep<LG, BS, true>(nitems, slots, srp, bcol, vals, invd, rhs, out, reset,
                                 static_cast<int64_t>(role) * (blockDim.x >> 5) + (threadIdx.x >> 5),
                                 static_cast<int64_t>(nsweep) * (blockDim.x >> 5), static_cast<unsigned>(tune >> 8),
                                 trace);

@@ -1,6 +1,4 @@
-# developer A/B: sweep knobs on configs[2]
 T="python tools/trsv_time.py elasticity_q1_118"
-PCLAB_FUSE=0 $T
-PCLAB_FUSE=0 PCLAB_TRSV_DEPTH=2 $T
-PCLAB_FUSE=0 PCLAB_TRSV_TRACE=/tmp/tr118 python tools/run_kernels.py elasticity_q1_118 0 1
-python tools/trace_trsv.py /tmp/tr118
+$T
+python tools/prof_stages.py elasticity_q1_118 0 3 2>&1 | grep -E "spmv|trsv|build warm"
+python tools/solve_var.py elasticity_q1_118 3 2>&1 | grep -E "run|eager"
