@@ -134,6 +134,11 @@ void pclab_precond_free(pclab_precond* p);
 pclab_status pclab_precond_info(const pclab_precond* p, int64_t* nnz_lower,
                                 int32_t* block_size, int32_t* levels_lower,
                                 int32_t* levels_upper, double* sigma);
+
+/* Device data layout of the sweeps and product (for traffic accounting):
+ * out8 = [node-blocked sweeps, node-blocked A, block columns of L, of U,
+ * of A, sweep slots lower, upper, lanes per block]. Zeros before analysis. */
+pclab_status pclab_precond_layout(const pclab_precond* p, int64_t* out8);
 /* Factor values in lower-triangle (row, col) order, as the reference's
  * LowerFactor stores them. Host or device destination. */
 pclab_status pclab_precond_factor(const pclab_precond* p, double* out);

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
                                         C.POINTER(C.c_void_p)]),
         "pclab_spmv_device": (st, [_vp, _vp, _vp, _vp]),
         "pclab_pcg_profile": (st, [_vp, _vp, _vp, _vp, C.c_int64, _f64p]),
+        "pclab_precond_layout": (st, [_vp, _i64p]),
         "pclab_set_stream": (None, [_vp]),
         "pclab_matrix_drop_analysis": (st, [_vp]),
         "pclab_launch_count": (C.c_longlong, []),
@@ -342,6 +343,14 @@ class Precond:
                                         C.byref(sg)))
         return {"nnz_lower": nl.value, "block_size": bs.value, "block_levels_lower": lo.value,
                 "block_levels_upper": up.value, "sigma": sg.value}
+
+    def layout(self) -> dict:
+        """Device layout of the sweeps and the product (pclab_precond_layout)."""
+        t = np.zeros(8, dtype=np.int64)
+        _check(lib().pclab_precond_layout(self._h, t))
+        return {"node_blocked": bool(t[0]), "a_node_blocked": bool(t[1]), "block_cols_lower": int(t[2]),
+                "block_cols_upper": int(t[3]), "block_cols_a": int(t[4]), "slots_lower": int(t[5]),
+                "slots_upper": int(t[6]), "lanes": int(t[7])}
 
     def factor(self) -> np.ndarray:
         out = np.empty(max(self.info()["nnz_lower"], 1))

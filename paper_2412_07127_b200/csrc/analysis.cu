@@ -413,9 +413,11 @@ void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, 
     CK(cudaStreamSynchronize(st));
     if (h.tail != static_cast<unsigned long long>(nb))
         throw FormatError("level analysis: dependency graph has a cycle");
-    crit_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, s.level.p,
-                                                   s.crit.p);
-    CK_LAUNCH();
+    if (s.need_crit) {
+        crit_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, s.level.p,
+                                                       s.crit.p);
+        CK_LAUNCH();
+    }
 }
 
 static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, int lanes,
@@ -741,6 +743,8 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     while (lanes < 32 && lanes < work) lanes *= 2;
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
     // (row-granular level sets are computed on request only: pclab_precond_levels)
+    // the critical-predecessor poll is the entry-lane sweep's (and traces')
+    an->blk_lo.need_crit = an->blk_up.need_crit = !an->bsr || getenv("PCLAB_TRSV_TRACE") != nullptr;
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
     build_schedule(U, L, bs, true, lanes, an->blk_up, st);
     if (an->bsr) {
@@ -759,7 +763,18 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
                 CK_LAUNCH();
             }
         }
-        if (dev_read(bad.p, st) != 0) an->bsr = false;  // a row too long for the packed record
+        if (dev_read(bad.p, st) != 0) {  // a row too long for the packed record: entry-lane sweep
+            an->bsr = false;
+            for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
+                if (sc->need_crit || sc->nblocks == 0) continue;
+                const bool up = sc == &an->blk_up;
+                const DevCsr& P = up ? U : L;
+                crit_kernel<<<grid_for(sc->nblocks, 256), 256, 0, st>>>(sc->nblocks, bs, P.rp.p, P.cols.p, up,
+                                                                        sc->level.p, sc->crit.p);
+                CK_LAUNCH();
+                sc->need_crit = true;
+            }
+        }
     }
     // node-blocked A: the PCG product reads one column index per block
     an->a_bsr = false;

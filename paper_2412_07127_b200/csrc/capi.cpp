@@ -622,6 +622,22 @@ pclab_status pclab_precond_info(const pclab_precond* p, int64_t* nnz_lower, int3
     return PCLAB_OK;
 }
 
+pclab_status pclab_precond_layout(const pclab_precond* p, int64_t* out8) {
+    if (p == nullptr || out8 == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_layout: null argument");
+    const Analysis* an = p->p->a->an.get();
+    for (int k = 0; k < 8; ++k) out8[k] = 0;
+    if (!an) return PCLAB_OK;
+    out8[0] = an->bsr ? 1 : 0;
+    out8[1] = an->a_bsr ? 1 : 0;
+    out8[2] = an->bsr ? an->lbc.bcol.n : 0;
+    out8[3] = an->bsr ? an->ubc.bcol.n : 0;
+    out8[4] = an->a_bsr ? an->abc.bcol.n : 0;
+    out8[5] = an->blk_lo.nitems * an->blk_lo.per_item;
+    out8[6] = an->blk_up.nitems * an->blk_up.per_item;
+    out8[7] = an->blk_lo.lanes;
+    return PCLAB_OK;
+}
+
 pclab_status pclab_precond_factor(const pclab_precond* p, double* out) {
     if (p == nullptr || out == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_factor: null argument");
     return guarded([&] {

@@ -77,7 +77,8 @@ struct Schedule {
     int32_t nlevels = 0;
     int64_t nitems = 0;
     DevBuf<int32_t> level;       // [nblocks] level of each block
-    DevBuf<int32_t> crit;        // [nblocks] row polled first (-1: no dependency)
+    DevBuf<int32_t> crit;        // [nblocks] row polled first (-1: no dependency; filled if need_crit)
+    bool need_crit = true;
     DevBuf<int32_t> order;       // [nblocks] blocks in schedule order
     DevBuf<int64_t> item_first;  // [nitems] first position in `order`
     DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item

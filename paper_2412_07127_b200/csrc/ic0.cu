@@ -132,11 +132,21 @@ ic0_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict__ slo
 
 __global__ void row_stats(int64_t n, const int64_t* __restrict__ rp, const double* __restrict__ lv,
                           unsigned* maxlen, unsigned long long* maxdiag) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    atomicMax(maxlen, static_cast<unsigned>(rp[i + 1] - rp[i]));
-    // |a_ii| >= 0: its IEEE bit pattern orders like an unsigned integer
-    atomicMax(maxdiag, static_cast<unsigned long long>(__double_as_longlong(fabs(lv[rp[i + 1] - 1]))));
+    unsigned ml = 0;
+    unsigned long long md = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        ml = max(ml, static_cast<unsigned>(rp[i + 1] - rp[i]));
+        // |a_ii| >= 0: its IEEE bit pattern orders like an unsigned integer
+        md = max(md, static_cast<unsigned long long>(__double_as_longlong(fabs(lv[rp[i + 1] - 1]))));
+    }
+    ml = __reduce_max_sync(0xffffffffu, ml);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(maxlen, ml);
+        atomicMax(maxdiag, md);
+    }
 }
 
 }  // namespace
@@ -150,7 +160,7 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
     DevBuf<unsigned long long> md(1);
     CK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned), st));
     CK(cudaMemsetAsync(md.p, 0, sizeof(unsigned long long), st));
-    row_stats<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, L.rp.p, L.vals.p, mx.p, md.p);
+    row_stats<<<static_cast<unsigned>(sm_count() * 4), 256, 0, st>>>(n, L.rp.p, L.vals.p, mx.p, md.p);
     CK_LAUNCH();
     unsigned maxlen = 0;
     unsigned long long mdbits = 0;
