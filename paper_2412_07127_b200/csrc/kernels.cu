@@ -35,7 +35,7 @@ spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict
     }
 }
 
-template <int BS, int R>
+template <int BS>
 __global__ void __launch_bounds__(256)
 spmv_bsr_kernel(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ x,
@@ -43,19 +43,19 @@ spmv_bsr_kernel(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t b0 = gw * R; b0 < nb; b0 += nw * R) {
-        double acc[R][BS];
-        bsr_block_dots<BS, R>(b0, nb, rp, bp, bcol, vals, x, acc);
-        if (lane < R * BS) {
-            const int j = lane / BS, t = lane % BS;
-            double v = 0.0;
+    BsrRow<BS> m = bsr_row<BS>(gw, nb, rp, bp);
+    for (int64_t b = gw; b < nb; b += nw) {
+        const BsrRow<BS> mn = bsr_row<BS>(b + nw, nb, rp, bp);
+        double acc[BS];
+        bsr_row_dot<BS>(m, bcol, vals, x, acc);
+        if (lane < BS) {
+            double v = acc[0];
 #pragma unroll
-            for (int jj = 0; jj < R; ++jj)
-#pragma unroll
-                for (int tt = 0; tt < BS; ++tt)
-                    if (jj == j && tt == t) v = acc[jj][tt];
-            if (b0 + j < nb) y[(b0 + j) * BS + t] = v;
+            for (int t = 1; t < BS; ++t)
+                if (lane == t) v = acc[t];
+            y[b * BS + lane] = v;
         }
+        m = mn;
     }
 }
 
@@ -75,6 +75,14 @@ int sm_count() {
         CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
     }
     return n;
+}
+
+// CTAs of `kernel` (256 threads) the whole GPU holds at once.
+template <typename K>
+static unsigned resident_ctas(K kernel) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+    return static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
 }
 
 void fill_pending(double* p, int64_t n, cudaStream_t st) {
@@ -100,10 +108,11 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
     const unsigned grid = static_cast<unsigned>(sm_count() * 8);
     if (a.an && a.an->a_bsr) {  // node-blocked: one column index per block
         const BlockCols& bc = a.an->abc;
+        static const unsigned g3 = resident_ctas(spmv_bsr_kernel<3>), g2 = resident_ctas(spmv_bsr_kernel<2>);
         if (a.an->bs == 3)
-            spmv_bsr_kernel<3, 2><<<grid, 256, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
+            spmv_bsr_kernel<3><<<g3, 256, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
         else
-            spmv_bsr_kernel<2, 2><<<grid, 256, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
+            spmv_bsr_kernel<2><<<g2, 256, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
         CK_LAUNCH();
         return;
     }
@@ -155,14 +164,6 @@ static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals
     trsv_kernel<LG, BS, UP><<<trsv_grid(s, 4.0), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
                                                           vals, invd, b, x, reset, done, ctr, trsv_tune(),
                                                           g_trace);
-}
-
-// CTAs of `kernel` (256 threads) the whole GPU holds at once.
-template <typename K>
-static unsigned resident_ctas(K kernel) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
-    return static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
 }
 
 // Round-robin items need every warp resident: the grid is capped at what

@@ -158,33 +158,32 @@ k_pq(int64_t n, const double* __restrict__ z, const double* __restrict__ w, doub
     }
 }
 
-// q = A p and pAp for a node-blocked A (Analysis::a_bsr): one warp per R
-// block rows, one column index per BSxBS block.
-template <int BS, int R>
+// q = A p and pAp for a node-blocked A (Analysis::a_bsr): warp per block
+// row (grid-stride), the next row's pointers loaded while this one runs.
+template <int BS>
 __global__ void __launch_bounds__(kT)
 k_spmv_bsr_pap(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
-               const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p,
-               double* __restrict__ q, Scal* S, double* part) {
+                const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p,
+                double* __restrict__ q, Scal* S, double* part) {
     if (S->done) return;
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * kT) >> 5;
     double loc = 0.0;
-    for (int64_t b0 = gw * R; b0 < nb; b0 += nw * R) {
-        double acc[R][BS];
-        bsr_block_dots<BS, R>(b0, nb, rp, bp, bcol, vals, p, acc);
+    BsrRow<BS> m = bsr_row<BS>(gw, nb, rp, bp);
+    for (int64_t b = gw; b < nb; b += nw) {
+        const BsrRow<BS> mn = bsr_row<BS>(b + nw, nb, rp, bp);
+        double acc[BS];
+        bsr_row_dot<BS>(m, bcol, vals, p, acc);
         if (lane == 0) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                if (b0 + j >= nb) break;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    const int64_t row = (b0 + j) * BS + t;
-                    q[row] = acc[j][t];
-                    loc = fma(p[row], acc[j][t], loc);
-                }
+            for (int t = 0; t < BS; ++t) {
+                const int64_t row = b * BS + t;
+                q[row] = acc[t];
+                loc = fma(p[row], acc[t], loc);
             }
         }
+        m = mn;
     }
     double tot;
     if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
@@ -489,6 +488,13 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK_LAUNCH();
     // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
+    auto one_wave = [](auto kernel) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kT, 0));
+        return static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+    };
+    static const unsigned bsr_grid3 = one_wave(k_spmv_bsr_pap<3>);
+    static const unsigned bsr_grid2 = one_wave(k_spmv_bsr_pap<2>);
     // `mark` runs after each of the five kernels (event hook for profiling)
     auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
         if (fused) {
@@ -507,13 +513,15 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         }
         k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
         if (an && an->a_bsr) {
+            // grid = one resident wave (grid-stride rows; a second partial
+            // wave doubles the tail: measured 0.75 vs 0.93 ms at 1.5 waves)
             const BlockCols& bc = an->abc;
             if (an->bs == 3)
-                k_spmv_bsr_pap<3, 2><<<sgrid, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
-                                                          S.p, part.p);
+                k_spmv_bsr_pap<3><<<bsr_grid3, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
+                                                           S.p, part.p);
             else
-                k_spmv_bsr_pap<2, 2><<<sgrid, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
-                                                          S.p, part.p);
+                k_spmv_bsr_pap<2><<<bsr_grid2, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
+                                                           S.p, part.p);
         } else switch (lpr) {
             case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;

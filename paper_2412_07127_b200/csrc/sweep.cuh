@@ -45,59 +45,52 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp,
     return group_sum<LPR>(acc);
 }
 
-// R consecutive block rows b0.. of a node-blocked matrix times x, one warp:
-// lane n owns neighbour block n of every row (32-wide rounds), all index
-// and value loads of the R rows are issued before the first x gather.
-// acc[j][t] = (A x)_{(b0 + j) BS + t}, valid in every lane.
-template <int BS, int R>
-__device__ __forceinline__ void bsr_block_dots(int64_t b0, int64_t nb, const int64_t* __restrict__ rp,
-                                               const int64_t* __restrict__ bp, const int32_t* __restrict__ bcol,
-                                               const double* __restrict__ vals, const double* __restrict__ x,
-                                               double (&acc)[R][BS]) {
+// Row pointers of block row b (node-blocked product), loaded one row ahead.
+template <int BS>
+struct BsrRow {
+    int64_t r[BS];
+    int64_t c0;
+    int cnt;
+};
+
+template <int BS>
+__device__ __forceinline__ BsrRow<BS> bsr_row(int64_t b, int64_t nb, const int64_t* __restrict__ rp,
+                                              const int64_t* __restrict__ bp) {
+    BsrRow<BS> m;
+    const bool ok = b < nb;
+#pragma unroll
+    for (int t = 0; t < BS; ++t) m.r[t] = ok ? __ldg(rp + b * BS + t) : 0;
+    m.c0 = ok ? __ldg(bp + b) : 0;
+    m.cnt = ok ? static_cast<int>(__ldg(bp + b + 1) - m.c0) : 0;
+    return m;
+}
+
+// (A x) for one block row whose pointers are in hand; lane n owns
+// neighbour block n (32-wide rounds). Result valid in every lane.
+template <int BS>
+__device__ __forceinline__ void bsr_row_dot(const BsrRow<BS>& m, const int32_t* __restrict__ bcol,
+                                            const double* __restrict__ vals, const double* __restrict__ x,
+                                            double (&acc)[BS]) {
     const int lane = threadIdx.x & 31;
-    int64_t r[R][BS], c0[R];
-    int cnt[R];
-    int cmax = 0;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-        const bool ok = b0 + j < nb;
+    for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+    for (int n = lane; n < m.cnt; n += 32) {
+        const int32_t xc = __ldg(bcol + m.c0 + n);
+        double a[BS][BS];
 #pragma unroll
-        for (int t = 0; t < BS; ++t) r[j][t] = ok ? __ldg(rp + (b0 + j) * BS + t) : 0;
-        c0[j] = ok ? __ldg(bp + b0 + j) : 0;
-        cnt[j] = ok ? static_cast<int>(__ldg(bp + b0 + j + 1) - c0[j]) : 0;
-        cmax = max(cmax, cnt[j]);
+        for (int t = 0; t < BS; ++t)
 #pragma unroll
-        for (int t = 0; t < BS; ++t) acc[j][t] = 0.0;
-    }
-    for (int n0 = 0; n0 < cmax; n0 += 32) {
-        const int n = n0 + lane;
-        double a[R][BS][BS];
-        int32_t xc[R];
+            for (int c = 0; c < BS; ++c) a[t][c] = __ldg(vals + m.r[t] + BS * n + c);
+        double xv[BS];
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const bool own = n < cnt[j];
-            xc[j] = own ? __ldg(bcol + c0[j] + n) : -1;
+        for (int c = 0; c < BS; ++c) xv[c] = __ldg(x + xc + c);
 #pragma unroll
-            for (int t = 0; t < BS; ++t)
+        for (int t = 0; t < BS; ++t)
 #pragma unroll
-                for (int c = 0; c < BS; ++c) a[j][t][c] = own ? __ldg(vals + r[j][t] + BS * n + c) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            if (xc[j] < 0) continue;
-            double xv[BS];
-#pragma unroll
-            for (int c = 0; c < BS; ++c) xv[c] = __ldg(x + xc[j] + c);
-#pragma unroll
-            for (int t = 0; t < BS; ++t)
-#pragma unroll
-                for (int c = 0; c < BS; ++c) acc[j][t] = fma(a[j][t][c], xv[c], acc[j][t]);
-        }
+            for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
     }
 #pragma unroll
-    for (int j = 0; j < R; ++j)
-#pragma unroll
-        for (int t = 0; t < BS; ++t) acc[j][t] = group_sum<32>(acc[j][t]);
+    for (int t = 0; t < BS; ++t) acc[t] = group_sum<32>(acc[t]);
 }
 
 // Per-item state of a sweep, loaded one item ahead.
