@@ -653,6 +653,133 @@ static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, c
     }
 }
 
+// ---------------------------------------------------------------- chains
+// Sweep-order index r of block b: lower sweeps run b = r, upper b = nb-1-r.
+// A block continues the chain of the block before it (in sweep order) when
+// that block is one of its neighbours: the last block column of an L block
+// row, the first of a U block row.
+__global__ void chain_starts(int64_t nb, int bs, bool upper, const int64_t* __restrict__ bp,
+                             const int32_t* __restrict__ bcol, int64_t* __restrict__ cs) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= nb) return;
+    const int64_t b = upper ? nb - 1 - r : r;
+    bool cont = false;
+    if (r > 0 && bp[b + 1] > bp[b]) {
+        const int64_t prev = upper ? b + 1 : b - 1;
+        const int32_t c = upper ? bcol[bp[b]] : bcol[bp[b + 1] - 1];
+        cont = static_cast<int64_t>(c) == prev * bs;
+    }
+    cs[r] = cont ? -1 : r;
+}
+
+struct MaxOp {
+    __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
+
+__global__ void seg_start_flags(int64_t nb, int k, const int64_t* __restrict__ cs, int64_t* __restrict__ flag) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r < nb) flag[r] = ((r - cs[r]) % k) == 0 ? 1 : 0;
+}
+
+// segment s starts at sweep index start[s]; key = (level of its first block, r)
+__global__ void seg_make(int64_t nb, bool upper, const int64_t* __restrict__ flag_incl,
+                         const int32_t* __restrict__ level, int64_t* __restrict__ start,
+                         unsigned long long* __restrict__ key, int32_t* __restrict__ sid) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= nb) return;
+    if (r == 0 || flag_incl[r] != flag_incl[r - 1]) {
+        const int64_t s = flag_incl[r] - 1;
+        start[s] = r;
+        const int64_t b = upper ? nb - 1 - r : r;
+        key[s] = (static_cast<unsigned long long>(level[b]) << 32) | static_cast<unsigned long long>(r);
+        sid[s] = static_cast<int32_t>(s);
+    }
+}
+
+// slots of the sorted segments; item of every block
+__global__ void seg_slots_fill(int64_t nseg, int64_t nb, int G, bool upper, const int32_t* __restrict__ sorted,
+                               const int64_t* __restrict__ start, int32_t* __restrict__ sfirst,
+                               int32_t* __restrict__ slen, int32_t* __restrict__ item_of) {
+    const int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (pos >= nseg) return;
+    const int32_t s = sorted[pos];
+    const int64_t r0 = start[s], r1 = s + 1 < nseg ? start[s + 1] : nb;
+    sfirst[pos] = static_cast<int32_t>(upper ? nb - 1 - r0 : r0);
+    slen[pos] = static_cast<int32_t>(r1 - r0);
+    for (int64_t r = r0; r < r1; ++r) item_of[upper ? nb - 1 - r : r] = static_cast<int32_t>(pos / G);
+}
+
+__global__ void chain_window(int64_t nb, int bs, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+                             const int32_t* __restrict__ bcol, const int32_t* __restrict__ item_of,
+                             unsigned long long* __restrict__ fwd, unsigned* __restrict__ maxnb,
+                             unsigned* __restrict__ maxblk) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    long long f = 0;
+    for (int64_t k = bp[b]; k < bp[b + 1]; ++k) f = max(f, static_cast<long long>(item_of[bcol[k] / bs]) - item_of[b]);
+    atomicMax(fwd, static_cast<unsigned long long>(f));
+    atomicMax(maxnb, static_cast<unsigned>(bp[b + 1] - bp[b]));
+    atomicMax(maxblk, static_cast<unsigned>(rp[(b + 1) * bs] - rp[b * bs]));
+}
+
+static void build_chains(const DevCsr& M, const BlockCols& bc, int bs, bool upper, int k, Schedule& s,
+                         cudaStream_t st) {
+    const int64_t nb = s.nblocks;
+    s.chain_k = k;
+    if (nb == 0) return;
+    DevBuf<int64_t> cs(nb), flag(nb);
+    chain_starts<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, upper, bc.bp.p, bc.bcol.p, cs.p);
+    CK_LAUNCH();
+    {
+        size_t tmp = 0;
+        cub::DeviceScan::InclusiveScan(nullptr, tmp, cs.p, cs.p, MaxOp(), nb, st);
+        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceScan::InclusiveScan(t.p, tmp, cs.p, cs.p, MaxOp(), nb, st);
+    }
+    seg_start_flags<<<grid_for(nb, 256), 256, 0, st>>>(nb, k, cs.p, flag.p);
+    CK_LAUNCH();
+    {
+        size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, flag.p, flag.p, nb, st);
+        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceScan::InclusiveSum(t.p, tmp, flag.p, flag.p, nb, st);
+    }
+    const int64_t nseg = dev_read(flag.p + nb - 1, st);
+    s.nseg = nseg;
+    DevBuf<int64_t> start(nseg);
+    DevBuf<unsigned long long> key(nseg), skey(nseg);
+    DevBuf<int32_t> sid(nseg), sorted(nseg);
+    seg_make<<<grid_for(nb, 256), 256, 0, st>>>(nb, upper, flag.p, s.level.p, start.p, key.p, sid.p);
+    CK_LAUNCH();
+    {
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, sid.p, sorted.p, static_cast<int>(nseg), 0, 64,
+                                        st);
+        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, sid.p, sorted.p, static_cast<int>(nseg), 0, 64, st);
+    }
+    const int G = 1;  // one segment per warp (chain_trsv_kernel)
+    s.chain_items = (nseg + G - 1) / G;
+    s.seg_first.alloc(s.chain_items * G);
+    s.seg_len.alloc(s.chain_items * G);
+    CK(cudaMemsetAsync(s.seg_first.p, 0xff, sizeof(int32_t) * s.chain_items * G, st));
+    CK(cudaMemsetAsync(s.seg_len.p, 0, sizeof(int32_t) * s.chain_items * G, st));
+    DevBuf<int32_t> item_of(nb);
+    seg_slots_fill<<<grid_for(nseg, 256), 256, 0, st>>>(nseg, nb, G, upper, sorted.p, start.p, s.seg_first.p,
+                                                        s.seg_len.p, item_of.p);
+    CK_LAUNCH();
+    DevBuf<unsigned long long> fwd(1);
+    DevBuf<unsigned> mnb(2);
+    CK(cudaMemsetAsync(fwd.p, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(mnb.p, 0, 2 * sizeof(unsigned), st));
+    chain_window<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, M.rp.p, bc.bp.p, bc.bcol.p, item_of.p, fwd.p, mnb.p,
+                                                    mnb.p + 1);
+    CK_LAUNCH();
+    s.chain_maxfwd = static_cast<int64_t>(dev_read(fwd.p, st));
+    s.chain_maxnb = static_cast<int32_t>(dev_read(mnb.p, st));
+    s.chain_maxblk = static_cast<int32_t>(dev_read(mnb.p + 1, st));
+}
+
 // A block rows sorted by the backward-sweep level that completes their z
 // inputs (Analysis::mv_order).
 static void build_mv_order(const DevCsr& A, Analysis& an, cudaStream_t st) {
@@ -762,6 +889,18 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
                                                                 (lo ? an->lbc : an->ubc).bp.p, sc->slot_rp.p, bad.p);
                 CK_LAUNCH();
             }
+        }
+        // whole chains by default: on a structured mesh every dependency of a
+        // pencil lies in a pencil that starts earlier (no window pressure)
+        // chain-segment sweep (chain.cuh): opt-in with PCLAB_CHAIN=1. On
+        // configs[2] it is slower than the round-robin node-blocked sweep
+        // (1.34 vs 0.99 ms): in-segment steps still pay an L2 re-poll for
+        // the just-in-time cross-segment dependencies
+        static const int chain_k = getenv("PCLAB_CHAIN_K") ? atoi(getenv("PCLAB_CHAIN_K")) : 128;
+        static const bool chain_on = getenv("PCLAB_CHAIN") && atoi(getenv("PCLAB_CHAIN")) != 0;
+        if (chain_on && chain_k > 0) {
+            build_chains(L, an->lbc, bs, false, chain_k, an->blk_lo, st);
+            build_chains(U, an->ubc, bs, true, chain_k, an->blk_up, st);
         }
         if (dev_read(bad.p, st) != 0) {  // a row too long for the packed record: entry-lane sweep
             an->bsr = false;

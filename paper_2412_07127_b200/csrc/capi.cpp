@@ -46,7 +46,8 @@ void* dev_alloc(size_t bytes) {
     }();
     (void)pool_ready;
     void* p = nullptr;
-    const cudaError_t e = cudaMallocAsync(&p, bytes, lib_stream());
+    // 64 bytes of slack: bulk copies (TMA) round ranges out to 16 bytes
+    const cudaError_t e = cudaMallocAsync(&p, bytes + 64, lib_stream());
     if (e != cudaSuccess) {
         cudaGetLastError();
         if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();

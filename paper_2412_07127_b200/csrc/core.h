@@ -85,6 +85,16 @@ struct Schedule {
     DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
     DevBuf<int64_t> slot_rp;     // [nitems * per_item * 4] {first row pointer, packed row lengths,
                                  //  block-column offset, 0} of the slot's block (bsr)
+    // chain segments (node-blocked sweeps): runs of consecutive blocks where
+    // each depends on the one before it in sweep order, cut at chain_k
+    // blocks, sorted by (level of the first block, index), one per warp
+    int64_t nseg = 0, chain_items = 0;
+    int chain_k = 0;
+    int64_t chain_maxfwd = -1;    // max (item of a dependency - item of the block)
+    int32_t chain_maxnb = 0;      // most neighbour blocks of one block
+    int32_t chain_maxblk = 0;     // most factor entries of one block (all its rows)
+    DevBuf<int32_t> seg_first;    // [chain_items] first block
+    DevBuf<int32_t> seg_len;      // [chain_items]
     int64_t max_level_width = 0;
     // chunked variant: contiguous chunks of `chunk_blocks` blocks, one CTA
     // each; inside a chunk, items of one local level (internal deps only)

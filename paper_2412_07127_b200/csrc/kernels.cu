@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "chain.cuh"
 #include "core.h"
 #include "sweep.cuh"
 
@@ -166,6 +167,38 @@ static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals
                                                           g_trace);
 }
 
+// Chain sweep (opt-in, PCLAB_CHAIN=1): used when the window condition holds
+// for the warps that fit (Schedule::chain_maxfwd < resident warps) and every
+// block has at most 32 neighbour blocks.
+template <int BS, bool UP>
+static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr& M, const double* vals,
+                           const double* invd, const double* b, double* x, double* reset, const int* done,
+                           cudaStream_t st) {
+    static const bool enabled = getenv("PCLAB_CHAIN") && atoi(getenv("PCLAB_CHAIN")) != 0;
+    if (!enabled || s.chain_items == 0 || s.chain_maxnb > 32 || s.chain_k > kChainMaxSeg) return false;
+    // bulk copies need 16-byte aligned sources (library buffers are)
+    for (const void* p : {static_cast<const void*>(vals), static_cast<const void*>(invd),
+                          static_cast<const void*>(b), static_cast<const void*>(bc.bcol.p)})
+        if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+    const ChainLayout lay = chain_layout(BS, s.chain_maxblk, s.chain_maxnb);
+    const size_t smem = 8 * static_cast<size_t>(lay.warp_bytes);
+    if (smem > 220 * 1024) return false;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        CK(cudaFuncSetAttribute(chain_tma_kernel<BS, UP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        smem_set = smem;
+    }
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_tma_kernel<BS, UP>, 256, smem));
+    const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * sm_count();
+    if (s.chain_maxfwd < 0 || s.chain_maxfwd >= cap * 8) return false;  // deadlock-freedom window
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(cap, (s.chain_items + 7) / 8));
+    chain_tma_kernel<BS, UP><<<grid, 256, smem, st>>>(s.chain_items, s.seg_first.p, s.seg_len.p, M.rp.p, bc.bp.p,
+                                                      bc.bcol.p, vals, invd, b, x, reset, done, lay, g_trace);
+    return true;
+}
+
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
 template <int LG, int BS, bool UP>
@@ -247,7 +280,7 @@ static void launch_tma_t(const Schedule& s, const unsigned char* pack, const dou
 }
 
 template <int BS, bool UP>
-static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const int32_t* bcol, const double* vals,
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const BlockCols* bc, const double* vals,
                            const double* invd, const unsigned char* pack, const double* b, double* x, double* reset,
                            const int* done, unsigned* ctr, cudaStream_t st) {
     if (sweep_mode() == 2 && pack && s.nchunks > 0 && s.pack_max_item <= kSlotBytes) {
@@ -271,7 +304,11 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const int32_t* bc
         return;
     }
     if constexpr (BS > 1) {
-        if (bcol) {
+        if (bc) {
+            const int32_t* bcol = bc->bcol.p;
+            bool chained = false;
+            chained = launch_chain_t<BS, UP>(s, *bc, M, vals, invd, b, x, reset, done, st);
+            if (chained) return;
             switch (s.lanes) {
             case 2:
             case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
@@ -298,7 +335,7 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, con
                  cudaStream_t st) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
-    const int32_t* bcol = an.bsr ? (upper ? an.ubc : an.lbc).bcol.p : nullptr;  // node-blocked sweep
+    const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
         if (an.bs == 3) launch_trsv_bs<3, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
@@ -342,11 +379,16 @@ void trsv(const Analysis& an, const double* vals, const double* invd, const unsi
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
     fill_pending(x, an.lower.n, st);
+    // the caller's right-hand side into a library buffer (aligned, padded:
+    // the chain sweep streams it with bulk copies)
+    DevBuf<double> bcopy(an.lower.n);
+    if (an.lower.n) CK(cudaMemcpyAsync(bcopy.p, b, sizeof(double) * an.lower.n, cudaMemcpyDeviceToDevice, st));
+    b = bcopy.p;
     const char* tf = getenv("PCLAB_TRSV_TRACE");
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     DevBuf<long long> tb;
     if (tf) {
-        tb.alloc(4 * (s.nitems + s.nchunks + s.cnitems));
+        tb.alloc(4 * (s.nitems * s.per_item + s.nchunks + s.cnitems + s.nblocks));
         g_trace = tb.p;
     }
     launch_trsv(an, vals, invd, pack, upper, b, x, nullptr, nullptr, ctr.p, st);

@@ -1,3 +1,3 @@
 T="python tools/trsv_time.py elasticity_q1_118"
-$T
-python tools/prof_stages.py elasticity_q1_118 0 3 2>&1 | grep -E "spmv|trsv"
+timeout 120 $T
+PCLAB_CHAIN=1 timeout 120 $T
