@@ -318,7 +318,7 @@ __global__ void slot_rp_fill(int64_t nslots, int bs, const int32_t* __restrict__
     }
     srp[4 * k] = r0;
     srp[4 * k + 1] = static_cast<int64_t>(lens);
-    srp[4 * k + 2] = b >= 0 ? bp[b] : 0;
+    srp[4 * k + 2] = b >= 0 && bp ? bp[b] : 0;
     srp[4 * k + 3] = 0;
 }
 
@@ -871,27 +871,47 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
     // (row-granular level sets are computed on request only: pclab_precond_levels)
     // the critical-predecessor poll is the entry-lane sweep's (and traces')
-    an->blk_lo.need_crit = an->blk_up.need_crit = !an->bsr || getenv("PCLAB_TRSV_TRACE") != nullptr;
+    // (round-robin sweeps need the slot records; PCLAB_RR=0 selects the
+    // claim-based entry-lane sweep for matrices that are not node-blocked)
+    static const bool rr_on = !(getenv("PCLAB_RR") && atoi(getenv("PCLAB_RR")) == 0);
+    an->blk_lo.need_crit = an->blk_up.need_crit =
+        (!an->bsr && !rr_on) || getenv("PCLAB_TRSV_TRACE") != nullptr;
     build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
     build_schedule(U, L, bs, true, lanes, an->blk_up, st);
     if (an->bsr) {
         build_block_cols(L, bs, 0, an->lbc, st);
         build_block_cols(U, bs, 1, an->ubc, st);
-        DevBuf<int> bad(1);
-        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    }
+    an->rr = false;
+    DevBuf<int> bad(1);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    if (an->bsr || rr_on) {
         for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
             const bool lo = sc == &an->blk_lo;
             const DevCsr& M = lo ? L : U;
             const int64_t ns = sc->nitems * sc->per_item;
             sc->slot_rp.alloc(std::max<int64_t>(4 * ns, 1));
             if (ns > 0) {
-                slot_rp_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, bs, sc->slots.p, M.rp.p,
-                                                                (lo ? an->lbc : an->ubc).bp.p, sc->slot_rp.p, bad.p);
+                slot_rp_fill<<<grid_for(ns, 256), 256, 0, st>>>(
+                    ns, bs, sc->slots.p, M.rp.p, an->bsr ? (lo ? an->lbc : an->ubc).bp.p : nullptr, sc->slot_rp.p,
+                    bad.p);
                 CK_LAUNCH();
             }
         }
-        // whole chains by default: on a structured mesh every dependency of a
-        // pencil lies in a pencil that starts earlier (no window pressure)
+        an->rr = !an->bsr && dev_read(bad.p, st) == 0;
+        if (!an->bsr && !an->rr) {
+            for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
+                if (sc->need_crit || sc->nblocks == 0) continue;
+                const bool up = sc == &an->blk_up;
+                const DevCsr& P = up ? U : L;
+                crit_kernel<<<grid_for(sc->nblocks, 256), 256, 0, st>>>(sc->nblocks, bs, P.rp.p, P.cols.p, up,
+                                                                        sc->level.p, sc->crit.p);
+                CK_LAUNCH();
+                sc->need_crit = true;
+            }
+        }
+    }
+    if (an->bsr) {
         // chain-segment sweep (chain.cuh): opt-in with PCLAB_CHAIN=1. On
         // configs[2] it is slower than the round-robin node-blocked sweep
         // (1.34 vs 0.99 ms): in-segment steps still pay an L2 re-poll for

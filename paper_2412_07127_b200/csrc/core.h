@@ -127,6 +127,7 @@ struct Analysis {
     DevBuf<int64_t> u2l;     // [nnz(U)] position in L of each U entry
     int bs = 1;              // detected dof block size (3 for elasticity)
     bool bsr = false;        // off-block pattern made of whole bs x bs blocks
+    bool rr = false;         // not node-blocked: round-robin entry-lane sweep (rr_trsv_kernel)
     BlockCols lbc, ubc;      // block columns of L / U (bsr)
     bool a_bsr = false;      // A itself node-blocked: product through abc
     BlockCols abc;

@@ -279,8 +279,17 @@ static void launch_tma_t(const Schedule& s, const unsigned char* pack, const dou
         s.nchunks, s.nblocks, s.chunk_blocks, s.chunk_item_ptr.p, pack, s.pack_off.p, b, x, reset, done, ctr);
 }
 
+template <int LG, int BS, bool UP, int CH>
+static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd, const double* b,
+                        double* x, double* reset, const int* done, cudaStream_t st) {
+    static const unsigned cap = resident_ctas(rr_trsv_kernel<LG, BS, UP, CH>);
+    const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
+    rr_trsv_kernel<LG, BS, UP, CH><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, M.cols.p, vals, invd, b,
+                                                          x, reset, done, trsv_tune());
+}
+
 template <int BS, bool UP>
-static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const BlockCols* bc, const double* vals,
+static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const BlockCols* bc, const double* vals,
                            const double* invd, const unsigned char* pack, const double* b, double* x, double* reset,
                            const int* done, unsigned* ctr, cudaStream_t st) {
     if (sweep_mode() == 2 && pack && s.nchunks > 0 && s.pack_max_item <= kSlotBytes) {
@@ -319,6 +328,16 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, const BlockCols* 
             return;
         }
     }
+    if (rr) {
+        switch (s.lanes) {
+            case 2:
+            case 4: launch_rr_t<4, BS, UP, 2>(s, M, vals, invd, b, x, reset, done, st); break;
+            case 8: launch_rr_t<8, BS, UP, 1>(s, M, vals, invd, b, x, reset, done, st); break;
+            case 16: launch_rr_t<16, BS, UP, 2>(s, M, vals, invd, b, x, reset, done, st); break;
+            default: launch_rr_t<32, BS, UP, 4>(s, M, vals, invd, b, x, reset, done, st); break;
+        }
+        return;
+    }
     switch (s.lanes) {
         case 2:
         case 4: launch_trsv_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
@@ -338,13 +357,13 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, con
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
     }
     CK_LAUNCH();
 }

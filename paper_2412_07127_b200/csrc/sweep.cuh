@@ -555,6 +555,171 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t
                              trace);
 }
 
+// Round-robin sweep for matrices that are not node-blocked (Poisson, FV
+// diffusion): the scheduling of bsr_sweep -- items dealt round-robin to all
+// resident warps, slot records two items ahead, entries prefetched into L1
+// one item ahead, dependency values polled directly -- with lanes over the
+// block's off-block entries (lane gl takes entries gl, gl + LG, ... of the
+// block's rows in order) instead of over neighbour blocks.
+template <int LG, int BS, bool UPPER, int CH>
+__global__ void __launch_bounds__(256, BSR_MINB)
+rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+               const int32_t* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ invd,
+               const double* rhs, double* out, double* reset, const int* __restrict__ done, int tune) {
+    if (done && *done) return;
+    constexpr int G = 32 / LG;
+    constexpr int NIB = BS * (BS - 1) / 2;
+    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    int64_t it = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    BsrSlot m = bsr_slot(it, nitems, G, grp, slots, srp);
+    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+    double rhs0[BS], rhs1[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) {
+        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
+        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+    }
+    auto prefetch = [&](const BsrSlot& q) {
+        if (q.blk >= 0) {
+            int64_t rq[BS + 1];
+            slot_rows<BS>(q, rq);
+            const int64_t e0 = rq[0], e1 = rq[BS];
+            for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
+            for (int64_t a = (e0 & ~31LL) + 32 * gl; a < e1; a += 32 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + a));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + static_cast<int64_t>(q.blk) * BS));
+        }
+    };
+    prefetch(m);
+    prefetch(m1);
+    while (it < nitems) {
+        prefetch(m2);
+        const bool active = m.blk >= 0;
+        const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
+        int64_t mrp[BS + 1];
+        slot_rows<BS>(m, mrp);
+        int64_t ob[BS];
+        int oc[BS];
+        int total = 0;
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
+            oc[t] = active ? static_cast<int>(UPPER ? mrp[t + 1] - ob[t] : mrp[t + 1] - (t + 1) - mrp[t]) : 0;
+            total += oc[t];
+        }
+        double binv[BS], bin[NIB > 0 ? NIB : 1];
+        if (active && gl == 0) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
+            int q = 0;
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int s = 0; s < BS; ++s) {
+                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
+                    if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
+                }
+        }
+        double acc[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+        const int tmax = __reduce_max_sync(0xffffffffu, total);
+        for (int base = 0; base < tmax; base += LG * CH) {
+            double v[CH], xv[CH];
+            int32_t jj[CH];
+            int tt[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                int e = base + c * LG + gl;
+                tt[c] = -1;
+                jj[c] = 0;
+                v[c] = 0.0;
+                xv[c] = 0.0;
+                if (e < total) {
+                    // row of entry e (selects, not a dynamically indexed array)
+                    int t = 0;
+                    int64_t obt = ob[0];
+#pragma unroll
+                    for (int s = 0; s < BS - 1; ++s)
+                        if (t == s && e >= oc[s]) {
+                            e -= oc[s];
+                            t = s + 1;
+                            obt = ob[s + 1];
+                        }
+                    tt[c] = t;
+                    jj[c] = ld_stream(cols + obt + e);
+                    v[c] = ld_stream(vals + obt + e);
+                    xv[c] = ld_relaxed(out + jj[c]);
+                }
+            }
+            bool pend = false;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
+            while (__any_sync(0xffffffffu, pend)) {
+                if (sleep_ns) __nanosleep(sleep_ns);
+                pend = false;
+#pragma unroll
+                for (int c = 0; c < CH; ++c)
+                    if (tt[c] >= 0 && is_pending(xv[c])) {
+                        xv[c] = ld_relaxed(out + jj[c]);
+                        pend |= is_pending(xv[c]);
+                    }
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+                    if (tt[c] == t) acc[t] = fma(v[c], xv[c], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+        if (active && gl == 0) {
+            double xb[BS];
+            if (!UPPER) {
+                int q = 0;
+#pragma unroll
+                for (int t = 0; t < BS; ++t) {
+                    double s = rhs0[t] - acc[t];
+#pragma unroll
+                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            } else {
+#pragma unroll
+                for (int t = BS - 1; t >= 0; --t) {
+                    double s = rhs0[t] - acc[t];
+                    int q = 0;
+#pragma unroll
+                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
+#pragma unroll
+                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+        }
+        __syncwarp();
+        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+        it += nwarps;
+        m = m1;
+        m1 = m2;
+        m2 = m3;
+        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            rhs0[t] = rhs1[t];
+            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+        }
+    }
+}
+
 // w = A z for node-blocked A, following the backward sweep's frontier: a
 // warp takes two block rows (in the order their z inputs complete,
 // Analysis::mv_order), lane n owns neighbour block n of both, polls its z
