@@ -194,11 +194,18 @@ chain_tma_kernel(int64_t nseg, const int32_t* __restrict__ sfirst, const int32_t
 #pragma unroll
                     for (int c = 0; c < BS; ++c) a[t][c] = own ? sv[ob + BS * lane + c] : 0.0;
                 }
-                // cross-segment dependencies: re-poll any still pending
+                // cross-segment dependencies: re-poll any still pending.
+                // (Measured: 95 % of steps find a dependency that was pending
+                // when loaded CK steps early -- the neighbour pencils run just
+                // in time -- and pay one L2 round trip here; refreshing the
+                // next step's values one step early halves that share but the
+                // refresh itself is then waited on: 1.45 vs 1.34 ms.)
                 bool pend = false;
 #pragma unroll
                 for (int c = 0; c < BS; ++c) pend |= own && !chain && is_pending(pxv[j][c]);
+                int repolls = 0;
                 while (__any_sync(0xffffffffu, pend)) {
+                    ++repolls;
                     pend = false;
 #pragma unroll
                     for (int c = 0; c < BS; ++c)
@@ -207,6 +214,8 @@ chain_tma_kernel(int64_t nseg, const int32_t* __restrict__ sfirst, const int32_t
                             pend |= is_pending(pxv[j][c]);
                         }
                 }
+                long long t_ready = 0;
+                if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
                 double acc[BS];
 #pragma unroll
                 for (int t = 0; t < BS; ++t) {
@@ -244,8 +253,8 @@ chain_tma_kernel(int64_t nseg, const int32_t* __restrict__ sfirst, const int32_t
                         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_pub));
                         trace[4 * b + 0] = t_start;
                         trace[4 * b + 1] = t_pub;
-                        trace[4 * b + 2] = I;
-                        trace[4 * b + 3] = s > 0 ? 1 : 0;
+                        trace[4 * b + 2] = t_ready;
+                        trace[4 * b + 3] = (s > 0 ? 1 : 0) | (min(repolls, 1000) << 1);
                     }
                 }
 #pragma unroll

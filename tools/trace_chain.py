@@ -1,25 +1,21 @@
 """Developer probe: per-block stamps of the chain sweep (PCLAB_TRSV_TRACE):
-[operands issued, published, item, in-chain] for every block."""
+[step start, dependencies in hand, published, in-chain | re-polls << 1]."""
 import sys
 
 import numpy as np
 
 for suf in (".lo", ".up"):
-    base = sys.argv[1] + suf
-    lv = np.fromfile(base + ".lev", dtype=np.int32)
-    t = np.fromfile(base, dtype=np.int64)
-    nb = int(sys.argv[2]) if len(sys.argv) > 2 else None
-    t = t.reshape(-1, 4)
-    pub = t[:, 1]
-    ok = pub > 0
+    t = np.fromfile(sys.argv[1] + suf, dtype=np.int64).reshape(-1, 4)
+    ok = t[:, 1] > 0
     t = t[ok]
     t0 = t[:, 0].min()
-    iss, pubt = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
-    step = pubt - iss
-    chain = t[:, 3] == 1
-    print(suf, "blocks", ok.sum(), "span us %.1f" % pubt.max())
-    print("  issue->publish: median %.2f p10 %.2f p90 %.2f us; in-chain %.2f, segment start %.2f"
-          % (np.median(step), np.percentile(step, 10), np.percentile(step, 90), np.median(step[chain]),
-             np.median(step[~chain])))
-    busy = np.array([((iss <= x) & (pubt >= x)).sum() for x in np.linspace(0, pubt.max(), 9)[1:-1]])
-    print("  blocks in flight at 1/8..7/8:", busy)
+    st, rd, pb = (t[:, 0] - t0) / 1e3, (t[:, 2] - t0) / 1e3, (t[:, 1] - t0) / 1e3
+    chain = (t[:, 3] & 1) == 1
+    rp = t[:, 3] >> 1
+    print(suf, "blocks", ok.sum(), "span us %.1f" % pb.max())
+    for name, m in (("all", np.ones_like(chain)), ("no re-poll", rp == 0), ("re-polled", rp > 0)):
+        if m.sum() == 0:
+            continue
+        print("  %-10s share %.2f  start->ready %.2f  ready->pub %.2f  (median us)"
+              % (name, m.mean(), np.median(rd[m] - st[m]), np.median(pb[m] - rd[m])))
+    print("  re-poll rounds when re-polled: median %d" % (np.median(rp[rp > 0]) if np.any(rp > 0) else 0))
