@@ -473,169 +473,6 @@ static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool 
     CK(cudaStreamSynchronize(st));
 }
 
-// ---------------------------------------------------------------- chunks
-// Local level of every block inside its chunk, counting only dependencies
-// that lie in the same chunk (one thread walks one chunk in sweep order).
-static __global__ void chunk_levels(int64_t nb, int bs, int64_t cb, const int64_t* __restrict__ prp,
-                                    const int32_t* __restrict__ pcols, bool upper,
-                                    int32_t* __restrict__ loc) {
-    const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    const int64_t b0 = c * cb;
-    if (b0 >= nb) return;
-    const int64_t b1 = min(nb, b0 + cb);
-    for (int64_t t = 0; t < b1 - b0; ++t) {
-        const int64_t b = upper ? b1 - 1 - t : b0 + t;
-        int lv = 0;
-        for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
-            for (int64_t k = prp[i]; k < prp[i + 1]; ++k) {
-                const int64_t jb = pcols[k] / bs;
-                if (jb >= b0 && jb < b1 && (upper ? jb > b : jb < b)) lv = max(lv, loc[jb] + 1);
-            }
-        loc[b] = lv;
-    }
-}
-
-static __global__ void chunk_keys(int64_t nb, int64_t cb, const int32_t* __restrict__ loc,
-                                  unsigned long long* __restrict__ key, int32_t* __restrict__ idx) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b >= nb) return;
-    key[b] = (static_cast<unsigned long long>(b / cb) << 32) | static_cast<unsigned>(loc[b]);
-    idx[b] = static_cast<int32_t>(b);
-}
-
-static __global__ void seg_starts(int64_t nb, const unsigned long long* __restrict__ key,
-                                  int64_t* __restrict__ flag) {
-    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (p < nb) flag[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
-}
-
-static __global__ void seg_fill(int64_t nb, const unsigned long long* __restrict__ key,
-                                const int64_t* __restrict__ incl /* inclusive scan of starts */,
-                                int64_t* __restrict__ seg_start) {
-    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (p < nb && (p == 0 || key[p] != key[p - 1])) seg_start[incl[p] - 1] = p;
-}
-
-static __global__ void seg_items(int64_t nseg, int64_t nb, int per_item, const int64_t* __restrict__ start,
-                                 int64_t* __restrict__ nit) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (s >= nseg) return;
-    const int64_t e = s + 1 < nseg ? start[s + 1] : nb;
-    nit[s] = (e - start[s] + per_item - 1) / per_item;
-}
-
-static __global__ void seg_slots(int64_t nseg, int64_t nb, int per_item, int64_t cb,
-                                 const int64_t* __restrict__ start, const int64_t* __restrict__ item0,
-                                 const int32_t* __restrict__ order, int32_t* __restrict__ slots,
-                                 int64_t* __restrict__ chunk_item_ptr) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (s >= nseg) return;
-    const int64_t b = start[s], e = s + 1 < nseg ? start[s + 1] : nb;
-    const int64_t c = order[b] / cb;
-    if (s == 0 || order[start[s - 1]] / cb != c) chunk_item_ptr[c] = item0[s];
-    int64_t it = item0[s];
-    for (int64_t p = b; p < e; p += per_item, ++it)
-        for (int g = 0; g < per_item; ++g) slots[it * per_item + g] = p + g < e ? order[p + g] : -1;
-}
-
-// Byte size of every packed item record (layout in sweep.cuh).
-static __global__ void pack_sizes(int64_t nitems, int G, int bs, bool upper, const int32_t* __restrict__ slots,
-                                  const int64_t* __restrict__ rp, int64_t* __restrict__ sz,
-                                  unsigned long long* __restrict__ maxsz) {
-    const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (k >= nitems) return;
-    int64_t nent = 0;
-    for (int g = 0; g < G; ++g) {
-        const int32_t blk = slots[k * G + g];
-        if (blk < 0) continue;
-        for (int t = 0; t < bs; ++t) {
-            const int64_t r = static_cast<int64_t>(blk) * bs + t;
-            nent += rp[r + 1] - rp[r] - (upper ? bs - t : t + 1);
-        }
-    }
-    const int nib = bs * (bs - 1) / 2;
-    const int64_t hdr = ((4LL * G * (1 + bs)) + 15) & ~15LL;
-    const int64_t b = hdr + ((4 * nent + 15) & ~15LL) + ((8 * nent + 15) & ~15LL) +
-                      ((8LL * G * (bs + nib) + 15) & ~15LL);
-    sz[k] = b;
-    atomicMax(maxsz, static_cast<unsigned long long>(b));
-}
-
-static void build_pack_layout(const DevCsr& M, int bs, bool upper, Schedule& s, cudaStream_t st) {
-    if (s.cnitems == 0) return;
-    s.pack_off.alloc(s.cnitems + 1);
-    DevBuf<unsigned long long> mx(1);
-    CK(cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), st));
-    pack_sizes<<<grid_for(s.cnitems, 256), 256, 0, st>>>(s.cnitems, s.per_item, bs, upper, s.cslots.p, M.rp.p,
-                                                        s.pack_off.p, mx.p);
-    CK_LAUNCH();
-    CK(cudaMemsetAsync(s.pack_off.p + s.cnitems, 0, sizeof(int64_t), st));
-    scan_inplace(s.pack_off.p, s.cnitems + 1, st);
-    s.pack_bytes = dev_read(s.pack_off.p + s.cnitems, st);
-    s.pack_max_item = static_cast<int64_t>(dev_read(mx.p, st));
-}
-
-// Contiguous chunks of `cb` blocks; inside each chunk the blocks are sorted
-// by (local level, index) and cut into warp items of one local level.
-static void build_chunk_schedule(const DevCsr& pred, int bs, bool upper, int64_t cb, Schedule& s,
-                                 cudaStream_t st) {
-    const int64_t nb = s.nblocks;
-    s.chunk_blocks = cb;
-    s.nchunks = (nb + cb - 1) / cb;
-    if (nb == 0) return;
-    DevBuf<int32_t> loc(nb), idx(nb);
-    DevBuf<unsigned long long> key(nb), skey(nb);
-    DevBuf<int32_t> order(nb);
-    chunk_levels<<<grid_for(s.nchunks, 64), 64, 0, st>>>(nb, bs, cb, pred.rp.p, pred.cols.p, upper, loc.p);
-    CK_LAUNCH();
-    chunk_keys<<<grid_for(nb, 256), 256, 0, st>>>(nb, cb, loc.p, key.p, idx.p);
-    CK_LAUNCH();
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, idx.p, order.p, static_cast<int>(nb), 0, 64,
-                                    st);
-    {
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, idx.p, order.p, static_cast<int>(nb), 0, 64,
-                                        st);
-        CK(cudaStreamSynchronize(st));
-    }
-    DevBuf<int64_t> flag(nb + 1);
-    seg_starts<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, flag.p);
-    CK_LAUNCH();
-    {
-        size_t t2 = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, t2, flag.p, flag.p, nb, st);
-        DevBuf<unsigned char> t(static_cast<int64_t>(t2) + 1);
-        cub::DeviceScan::InclusiveSum(t.p, t2, flag.p, flag.p, nb, st);
-        CK(cudaStreamSynchronize(st));
-    }
-    const int64_t nseg = dev_read(flag.p + nb - 1, st);
-    DevBuf<int64_t> start(nseg), nit(nseg + 1);
-    seg_fill<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, flag.p, start.p);
-    CK_LAUNCH();
-    seg_items<<<grid_for(nseg, 256), 256, 0, st>>>(nseg, nb, s.per_item, start.p, nit.p);
-    CK_LAUNCH();
-    CK(cudaMemsetAsync(nit.p + nseg, 0, sizeof(int64_t), st));
-    scan_inplace(nit.p, nseg + 1, st);
-    s.cnitems = dev_read(nit.p + nseg, st);
-    s.cslots.alloc(s.cnitems * s.per_item);
-    s.chunk_item_ptr.alloc(s.nchunks + 1);
-    CK(cudaMemcpyAsync(s.chunk_item_ptr.p + s.nchunks, nit.p + nseg, sizeof(int64_t), cudaMemcpyDeviceToDevice,
-                       st));
-    seg_slots<<<grid_for(nseg, 128), 128, 0, st>>>(nseg, nb, s.per_item, cb, start.p, nit.p, order.p,
-                                                   s.cslots.p, s.chunk_item_ptr.p);
-    CK_LAUNCH();
-    // deepest chunk-local level chain (reported)
-    {
-        std::vector<int32_t> h(nb);
-        CK(cudaMemcpyAsync(h.data(), loc.p, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        int32_t mx = 0;
-        for (int32_t v : h) mx = std::max(mx, v);
-        s.max_local_levels = mx + 1;
-    }
-}
-
 static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, cudaStream_t st) {
     const int64_t nb = M.n / bs;
     bc.bp.alloc(nb + 1);
@@ -652,6 +489,7 @@ static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, c
         CK_LAUNCH();
     }
 }
+
 
 // ---------------------------------------------------------------- chains
 // Sweep-order index r of block b: lower sweeps run b = r, upper b = nb-1-r.
@@ -954,16 +792,6 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     if (an->a_bsr && getenv("PCLAB_FUSE") && atoi(getenv("PCLAB_FUSE")) != 0) {
         build_mv_order(a, *an, st);
         an->fused_up = true;
-    }
-    // chunked / TMA-fed sweeps (experimental, PCLAB_SWEEP=1|2): their
-    // schedules and packed streams are only built when selected
-    if (getenv("PCLAB_SWEEP") && atoi(getenv("PCLAB_SWEEP")) != 0) {
-        static const int64_t chunk_rows = getenv("PCLAB_CHUNK_ROWS") ? atoll(getenv("PCLAB_CHUNK_ROWS")) : 3072;
-        const int64_t cb = std::max<int64_t>(1, std::min<int64_t>(chunk_rows, kMaxChunkRows) / bs);
-        build_chunk_schedule(L, bs, false, cb, an->blk_lo, st);
-        build_chunk_schedule(U, bs, true, cb, an->blk_up, st);
-        build_pack_layout(L, bs, false, an->blk_lo, st);
-        build_pack_layout(U, bs, true, an->blk_up, st);
     }
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));

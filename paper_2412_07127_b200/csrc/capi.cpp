@@ -763,7 +763,7 @@ pclab_status pclab_trsv_device(const pclab_precond* p, int upper, const double* 
         const Analysis* an = p->p->a->an.get();
         if (!an || p->p->lvals.n == 0) throw DimensionError("preconditioner has no factor");
         trsv(*an, upper ? p->p->uvals.p : p->p->lvals.p, p->p->invd.p,
-             upper ? p->p->pack_up.p : p->p->pack_lo.p, upper != 0, b, x, as_stream(stream));
+             upper != 0, b, x, as_stream(stream));
     });
 }
 

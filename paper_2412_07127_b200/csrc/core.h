@@ -14,8 +14,6 @@
 
 namespace pclab_b200 {
 
-// Largest row chunk of the chunked sweeps (its values live in shared memory).
-constexpr int64_t kMaxChunkRows = 6144;
 
 cudaStream_t lib_stream();
 void* dev_alloc(size_t bytes);  // stream-ordered on lib_stream(), pooled
@@ -96,15 +94,6 @@ struct Schedule {
     DevBuf<int32_t> seg_first;    // [chain_items] first block
     DevBuf<int32_t> seg_len;      // [chain_items]
     int64_t max_level_width = 0;
-    // chunked variant: contiguous chunks of `chunk_blocks` blocks, one CTA
-    // each; inside a chunk, items of one local level (internal deps only)
-    int64_t chunk_blocks = 0, nchunks = 0, cnitems = 0;
-    int32_t max_local_levels = 0;
-    DevBuf<int64_t> chunk_item_ptr;  // [nchunks + 1]
-    DevBuf<int32_t> cslots;          // [cnitems * per_item]
-    // packed stream (TMA sweep): item k occupies bytes [pack_off[k], pack_off[k+1])
-    DevBuf<int64_t> pack_off;        // [cnitems + 1]
-    int64_t pack_bytes = 0, pack_max_item = 0;
 };
 
 // Block-column view of a node-blocked CSR matrix (Analysis::bsr): block
@@ -163,7 +152,6 @@ struct Precond {
     DevBuf<double> lvals;       // factor values on L's pattern
     DevBuf<double> uvals;       // same values on U's pattern (gathered)
     DevBuf<double> invd;        // 1 / l_ii (both sweeps)
-    DevBuf<unsigned char> pack_lo, pack_up;  // schedule-ordered factor streams (TMA sweeps)
     DevBuf<double> diag;        // Jacobi payload
     double sigma = 1.0;         // GNN edge scale
     int ic0_attempts = 0;
@@ -211,17 +199,14 @@ void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* ou
 
 // kernels.cu
 void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
-void trsv(const Analysis& an, const double* vals, const double* invd, const unsigned char* pack,
-          bool upper, const double* b, double* x, cudaStream_t st);
-void launch_trsv(const Analysis& an, const double* vals, const double* invd, const unsigned char* pack,
-                 bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                 cudaStream_t st);
+void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
+          cudaStream_t st);
+void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
+                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st);
 // Backward sweep z = U^-1 y fused with w = A z (Analysis::fused_up).
 void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
                        const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
                        cudaStream_t st);
-void pack_factor(const Analysis& an, const double* lvals, const double* uvals, const double* invd,
-                 DevBuf<unsigned char>& plo, DevBuf<unsigned char>& pup, cudaStream_t st);
 void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);
 int spmv_lanes(const Matrix& a);
 void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st);

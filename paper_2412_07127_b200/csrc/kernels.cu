@@ -228,57 +228,6 @@ static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uv
         an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
 }
 
-// PCLAB_SWEEP=0 selects the warp-item sweep (global level order), default
-// 1 the chunked sweep.
-static int sweep_mode() {
-    static const int m = getenv("PCLAB_SWEEP") ? atoi(getenv("PCLAB_SWEEP")) : 0;
-    return m;
-}
-
-template <int LG, int BS, bool UP>
-static void launch_chunk_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
-                           const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                           cudaStream_t st) {
-    constexpr int kThreads = 512;
-    const size_t smem = static_cast<size_t>(s.chunk_blocks) * BS * sizeof(double);
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        CK(cudaFuncSetAttribute(chunk_trsv_kernel<LG, BS, UP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kMaxChunkRows * sizeof(double))));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_trsv_kernel<LG, BS, UP>, kThreads,
-                                                         kMaxChunkRows * sizeof(double)));
-        per_sm = std::max(per_sm, 1);
-    }
-    const int64_t grid = std::min<int64_t>(s.nchunks, static_cast<int64_t>(sm_count()) * per_sm);
-    chunk_trsv_kernel<LG, BS, UP><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(
-        s.nchunks, s.nblocks, s.chunk_blocks, s.chunk_item_ptr.p, s.cslots.p, M.rp.p, M.cols.p, vals, invd, b, x,
-        reset, done, ctr, g_trace);
-}
-
-constexpr int kRingSlots = 32;
-constexpr int kSlotBytes = 2048;
-
-template <int LG, int BS, bool UP>
-static void launch_tma_t(const Schedule& s, const unsigned char* pack, const double* b, double* x,
-                         double* reset, const int* done, unsigned* ctr, cudaStream_t st) {
-    constexpr int kThreads = 512;
-    const size_t smem = static_cast<size_t>(kRingSlots) * kSlotBytes + 2 * kRingSlots * sizeof(uint64_t) +
-                        static_cast<size_t>(s.chunk_blocks) * BS * sizeof(double);
-    constexpr size_t kMaxSmem = static_cast<size_t>(kRingSlots) * kSlotBytes + 2 * kRingSlots * sizeof(uint64_t) +
-                                kMaxChunkRows * sizeof(double);
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        CK(cudaFuncSetAttribute(tma_trsv_kernel<LG, BS, UP, kRingSlots, kSlotBytes>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxSmem)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tma_trsv_kernel<LG, BS, UP, kRingSlots, kSlotBytes>,
-                                                         kThreads, smem));
-        per_sm = std::max(per_sm, 1);
-    }
-    const int64_t grid = std::min<int64_t>(s.nchunks, static_cast<int64_t>(sm_count()) * per_sm);
-    tma_trsv_kernel<LG, BS, UP, kRingSlots, kSlotBytes><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(
-        s.nchunks, s.nblocks, s.chunk_blocks, s.chunk_item_ptr.p, pack, s.pack_off.p, b, x, reset, done, ctr);
-}
-
 template <int LG, int BS, bool UP, int CH>
 static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd, const double* b,
                         double* x, double* reset, const int* done, cudaStream_t st) {
@@ -290,28 +239,8 @@ static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, 
 
 template <int BS, bool UP>
 static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const BlockCols* bc, const double* vals,
-                           const double* invd, const unsigned char* pack, const double* b, double* x, double* reset,
-                           const int* done, unsigned* ctr, cudaStream_t st) {
-    if (sweep_mode() == 2 && pack && s.nchunks > 0 && s.pack_max_item <= kSlotBytes) {
-        switch (s.lanes) {
-            case 2:
-            case 4: launch_tma_t<4, BS, UP>(s, pack, b, x, reset, done, ctr, st); break;
-            case 8: launch_tma_t<8, BS, UP>(s, pack, b, x, reset, done, ctr, st); break;
-            case 16: launch_tma_t<16, BS, UP>(s, pack, b, x, reset, done, ctr, st); break;
-            default: launch_tma_t<32, BS, UP>(s, pack, b, x, reset, done, ctr, st); break;
-        }
-        return;
-    }
-    if (sweep_mode() == 1 && s.nchunks > 0) {
-        switch (s.lanes) {
-            case 2:
-            case 4: launch_chunk_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            case 8: launch_chunk_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            case 16: launch_chunk_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-            default: launch_chunk_t<32, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
-        }
-        return;
-    }
+                           const double* invd, const double* b, double* x, double* reset, const int* done,
+                           unsigned* ctr, cudaStream_t st) {
     if constexpr (BS > 1) {
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
@@ -349,21 +278,20 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
 
 // Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
 // with kPending) and the optional reset buffer.
-void launch_trsv(const Analysis& an, const double* vals, const double* invd, const unsigned char* pack,
-                 bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
+void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
                  cudaStream_t st) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, pack, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
     }
     CK_LAUNCH();
 }
@@ -393,7 +321,7 @@ void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals,
     CK_LAUNCH();
 }
 
-void trsv(const Analysis& an, const double* vals, const double* invd, const unsigned char* pack, bool upper,
+void trsv(const Analysis& an, const double* vals, const double* invd, bool upper,
           const double* b, double* x, cudaStream_t st) {
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
@@ -407,10 +335,10 @@ void trsv(const Analysis& an, const double* vals, const double* invd, const unsi
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     DevBuf<long long> tb;
     if (tf) {
-        tb.alloc(4 * (s.nitems * s.per_item + s.nchunks + s.cnitems + s.nblocks));
+        tb.alloc(4 * (s.nitems * s.per_item + s.nblocks));
         g_trace = tb.p;
     }
-    launch_trsv(an, vals, invd, pack, upper, b, x, nullptr, nullptr, ctr.p, st);
+    launch_trsv(an, vals, invd, upper, b, x, nullptr, nullptr, ctr.p, st);
     CK(cudaStreamSynchronize(st));
     g_trace = nullptr;
     if (tf) {
@@ -440,83 +368,6 @@ void trsv(const Analysis& an, const double* vals, const double* invd, const unsi
         dump(path + ".lev", il);
         dump(path + ".slots", sl);
         dump(path + ".crit", cr);
-    }
-}
-
-// Writes the packed item records of one sweep (layout in sweep.cuh): warp
-// per item, entries copied in (block, row, CSR) order.
-__global__ void pack_kernel(int64_t nitems, int G, int bs, bool upper, const int32_t* __restrict__ slots,
-                            const int64_t* __restrict__ rp, const int32_t* __restrict__ mcols,
-                            const double* __restrict__ mvals, const double* __restrict__ invd,
-                            const int64_t* __restrict__ off, unsigned char* __restrict__ pack) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int nib = bs * (bs - 1) / 2;
-    for (int64_t k = w0; k < nitems; k += nw) {
-        unsigned char* rec = pack + off[k];
-        int32_t* hdr = reinterpret_cast<int32_t*>(rec);
-        int64_t ntot = 0;
-        for (int g = 0; g < G; ++g) {
-            const int32_t blk = slots[k * G + g];
-            if (blk < 0) continue;
-            for (int t = 0; t < bs; ++t) {
-                const int64_t r = static_cast<int64_t>(blk) * bs + t;
-                ntot += rp[r + 1] - rp[r] - (upper ? bs - t : t + 1);
-            }
-        }
-        const int64_t H = pack_hdr_bytes(G, bs);
-        int32_t* rcols = reinterpret_cast<int32_t*>(rec + H);
-        double* rvals = reinterpret_cast<double*>(rec + H + align16(4 * ntot));
-        double* rdiag = reinterpret_cast<double*>(rec + H + align16(4 * ntot) + align16(8 * ntot));
-        int64_t pos = 0;
-        for (int g = 0; g < G; ++g) {
-            const int32_t blk = slots[k * G + g];
-            if (lane == 0) hdr[g * (1 + bs)] = blk;
-            for (int t = 0; t < bs; ++t) {
-                if (blk < 0) {
-                    if (lane == 0) hdr[g * (1 + bs) + 1 + t] = 0;
-                    continue;
-                }
-                const int64_t r = static_cast<int64_t>(blk) * bs + t;
-                const int64_t rb = rp[r], re = rp[r + 1];
-                const int64_t ob = upper ? rb + (bs - t) : rb;
-                const int64_t oc = upper ? re - ob : re - (t + 1) - rb;
-                if (lane == 0) hdr[g * (1 + bs) + 1 + t] = static_cast<int32_t>(oc);
-                for (int64_t e = lane; e < oc; e += 32) {
-                    rcols[pos + e] = mcols[ob + e];
-                    rvals[pos + e] = mvals[ob + e];
-                }
-                pos += oc;
-            }
-            if (lane == 0 && blk >= 0) {
-                double* d = rdiag + g * (bs + nib);
-                const int64_t r0 = static_cast<int64_t>(blk) * bs;
-                for (int t = 0; t < bs; ++t) d[t] = invd[r0 + t];
-                int q = 0;
-                for (int t = 0; t < bs; ++t)
-                    for (int s2 = 0; s2 < bs; ++s2) {
-                        if (!upper && s2 < t) d[bs + q++] = mvals[rp[r0 + t + 1] - (t + 1) + s2];
-                        if (upper && s2 > t) d[bs + q++] = mvals[rp[r0 + t] + (s2 - t)];
-                    }
-            }
-        }
-    }
-}
-
-void pack_factor(const Analysis& an, const double* lvals, const double* uvals, const double* invd,
-                 DevBuf<unsigned char>& plo, DevBuf<unsigned char>& pup, cudaStream_t st) {
-    const Schedule* ss[2] = {&an.blk_lo, &an.blk_up};
-    DevBuf<unsigned char>* outs[2] = {&plo, &pup};
-    const DevCsr* ms[2] = {&an.lower, &an.upper};
-    const double* vs[2] = {lvals, uvals};
-    for (int d = 0; d < 2; ++d) {
-        const Schedule& s = *ss[d];
-        if (s.cnitems == 0 || s.pack_bytes == 0) continue;
-        outs[d]->alloc(s.pack_bytes);
-        pack_kernel<<<sm_count() * 8, 256, 0, st>>>(s.cnitems, s.per_item, an.bs, d == 1, s.cslots.p, ms[d]->rp.p,
-                                                    ms[d]->cols.p, vs[d], invd, s.pack_off.p, outs[d]->p);
-        CK_LAUNCH();
     }
 }
 

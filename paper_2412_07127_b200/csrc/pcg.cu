@@ -396,7 +396,6 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
     gather_upper(an, p->lvals.p, p->uvals.p, st);
     p->invd.alloc(n);
     reciprocal_diag(an, p->lvals.p, p->invd.p, st);
-    pack_factor(an, p->lvals.p, p->uvals.p, p->invd.p, p->pack_lo, p->pack_up, st);
     p->ms_total = total.ms();  // the analysis ran inside this interval
     return p;
 }
@@ -471,11 +470,11 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         Timer tt(st);
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
             if (fused)
                 launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, nullptr, S.p->ctr + 1, st);
             else
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, pc.pack_up.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
@@ -503,7 +502,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             mark();
             k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
             mark();
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
             mark();
             launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, &S.p->done, S.p->ctr + 1, st);
             mark();
@@ -537,9 +536,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
         mark();
         if (factor) {
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, pc.pack_lo.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
             mark();
-            launch_trsv(*an, pc.uvals.p, pc.invd.p, pc.pack_up.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
             mark();
         } else {
             if (pc.kind == Kind::Jacobi) k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);

@@ -861,22 +861,7 @@ bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int
 }
 
 // ------------------------------------------------------------------------
-// Packed schedule-ordered factor stream (the TMA sweep's input). Item k of
-// the chunk schedule (G blocks of BS rows, one chunk-local level) is one
-// contiguous, 16-byte aligned record:
-//   int32 hdr[G][1 + BS]     block id (-1 idle), off-block entry count per row
-//   int32 cols[nent]          off-block column indices (block, row, CSR order)
-//   fp64  vals[nent]          their factor values
-//   fp64  diag[G][BS + NIB]   reciprocal pivots, then the strictly triangular
-//                             in-block entries (row-major)
-// so one bulk copy brings everything an item needs into shared memory.
-__host__ __device__ __forceinline__ int64_t align16(int64_t x) { return (x + 15) & ~static_cast<int64_t>(15); }
-__host__ __device__ __forceinline__ int64_t pack_hdr_bytes(int G, int bs) { return align16(4LL * G * (1 + bs)); }
-__host__ __device__ __forceinline__ int64_t pack_item_bytes(int G, int bs, int64_t nent) {
-    const int nib = bs * (bs - 1) / 2;
-    return pack_hdr_bytes(G, bs) + align16(4 * nent) + align16(8 * nent) + align16(8LL * G * (bs + nib));
-}
-
+// mbarrier / bulk-copy helpers (chain.cuh)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -906,412 +891,6 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
             smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
-}
-
-// TMA-fed chunked sweep.
-//
-// Persistent CTAs claim row chunks in sweep order. Warp 0 lane 0 is the
-// producer: it streams the chunk's packed item records into a ring of RS
-// shared-memory slots with 1-D bulk copies (cp.async.bulk, completion on a
-// per-slot mbarrier) running up to RS items ahead. The other warps consume
-// items round-robin: their entries, values and pivots come from shared
-// memory, internal dependencies from the chunk's shared-memory solution
-// block (~70 ns handoff), external ones from L2 (~400 ns, issued as soon as
-// the item is in hand). The L stream is read once, sequentially, by TMA.
-template <int LG, int BS, bool UPPER, int RS, int SLOT>
-__global__ void __launch_bounds__(512)
-tma_trsv_kernel(int64_t nchunks, int64_t nb, int64_t cb, const int64_t* __restrict__ chunk_item_ptr,
-                const unsigned char* __restrict__ pack, const int64_t* __restrict__ pack_off,
-                const double* rhs, double* out, double* reset, const int* __restrict__ done,
-                unsigned* counter) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int G = 32 / LG;
-    constexpr int NIB = BS * (BS - 1) / 2;
-    constexpr int CH = SLOT / 12 / LG + 1;  // entries per lane (upper bound)
-    unsigned char* ring = smem_raw;                                     // RS * SLOT
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + RS * SLOT);     // RS
-    uint64_t* empty = full + RS;                                        // RS
-    volatile double* xs = reinterpret_cast<volatile double*>(empty + RS);  // cb * BS
-    __shared__ unsigned s_claim;
-    if (done && *done) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ncons = (blockDim.x >> 5) - 1;
-    const int grp = lane / LG, gl = lane % LG;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < RS; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint64_t q0 = 0;  // ring sequence number of the chunk's first item
-    for (;;) {
-        if (threadIdx.x == 0) s_claim = atomicAdd(counter, 1u);
-        __syncthreads();
-        const unsigned claim = s_claim;
-        if (claim >= nchunks) return;
-        const int64_t c = UPPER ? nchunks - 1 - static_cast<int64_t>(claim) : static_cast<int64_t>(claim);
-        const int64_t b0 = c * cb, b1 = min(nb, b0 + cb);
-        const int64_t c0 = b0 * BS, c1 = b1 * BS;
-        const int64_t ib = chunk_item_ptr[c], ie = chunk_item_ptr[c + 1];
-        for (int64_t i = threadIdx.x; i < c1 - c0; i += blockDim.x) xs[i] = pending_value();
-        __syncthreads();
-        if (warp == 0) {
-            if (lane == 0) {
-                for (int64_t j = 0; j < ie - ib; ++j) {
-                    const uint64_t q = q0 + j;
-                    const int s = static_cast<int>(q % RS);
-                    mbar_wait(empty + s, static_cast<unsigned>(((q / RS) & 1) ^ 1));
-                    const int64_t o0 = pack_off[ib + j], o1 = pack_off[ib + j + 1];
-                    const unsigned bytes = static_cast<unsigned>(o1 - o0);
-                    mbar_arrive_expect_tx(full + s, bytes);
-                    tma_bulk_g2s(ring + static_cast<size_t>(s) * SLOT, pack + o0, bytes, full + s);
-                }
-            }
-        } else {
-            for (int64_t j = warp - 1; j < ie - ib; j += ncons) {
-                const uint64_t q = q0 + j;
-                const int s = static_cast<int>(q % RS);
-                mbar_wait(full + s, static_cast<unsigned>((q / RS) & 1));
-                const unsigned char* rec = ring + static_cast<size_t>(s) * SLOT;
-                const int32_t* hdr = reinterpret_cast<const int32_t*>(rec);
-                // offsets of this lane group's block inside the record
-                int ntot = 0, nbefore = 0;
-                int oc[BS];
-#pragma unroll
-                for (int g = 0; g < G; ++g)
-#pragma unroll
-                    for (int t = 0; t < BS; ++t) {
-                        const int v = hdr[g * (1 + BS) + 1 + t];
-                        if (g < grp) nbefore += v;
-                        if (g == grp) oc[t] = v;
-                        ntot += v;
-                    }
-                const int32_t blk = hdr[grp * (1 + BS)];
-                const bool active = blk >= 0;
-                const int64_t r0 = active ? static_cast<int64_t>(blk) * BS : c0;
-                const int64_t H = pack_hdr_bytes(G, BS);
-                const int32_t* rcols = reinterpret_cast<const int32_t*>(rec + H);
-                const double* rvals = reinterpret_cast<const double*>(rec + H + align16(4LL * ntot));
-                const double* rdiag =
-                    reinterpret_cast<const double*>(rec + H + align16(4LL * ntot) + align16(8LL * ntot)) +
-                    grp * (BS + NIB);
-                int total = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) total += active ? oc[t] : 0;
-                double brhs[BS];
-                if (active && gl == 0) {
-#pragma unroll
-                    for (int t = 0; t < BS; ++t) brhs[t] = rhs[r0 + t];
-                }
-                double acc[BS];
-#pragma unroll
-                for (int t = 0; t < BS; ++t) acc[t] = 0.0;
-                const int tmax = __reduce_max_sync(0xffffffffu, total);  // uniform trip count
-                for (int base = 0; base < tmax; base += LG * CH) {
-                    double v[CH], xv[CH];
-                    int32_t jj[CH];
-                    int tt[CH];
-                    bool ext[CH];
-#pragma unroll
-                    for (int cc = 0; cc < CH; ++cc) {
-                        const int e = base + cc * LG + gl;
-                        tt[cc] = -1;
-                        jj[cc] = 0;
-                        v[cc] = 0.0;
-                        ext[cc] = false;
-                        if (e < total) {
-                            int t = 0, rem = e;
-#pragma unroll
-                            for (int u = 0; u < BS - 1; ++u)
-                                if (t == u && rem >= oc[u]) {
-                                    rem -= oc[u];
-                                    t = u + 1;
-                                }
-                            tt[cc] = t;
-                            jj[cc] = rcols[nbefore + e];
-                            v[cc] = rvals[nbefore + e];
-                            ext[cc] = UPPER ? jj[cc] >= c1 : jj[cc] < c0;
-                        }
-                    }
-#pragma unroll
-                    for (int cc = 0; cc < CH; ++cc)
-                        xv[cc] = tt[cc] < 0 ? 0.0 : (ext[cc] ? ld_relaxed(out + jj[cc]) : xs[jj[cc] - c0]);
-                    // warp-uniform spin: divergent per-lane spin loops let the
-                    // scheduler park the waiting half of the warp for microseconds
-                    bool pend = false;
-#pragma unroll
-                    for (int cc = 0; cc < CH; ++cc) pend |= tt[cc] >= 0 && is_pending(xv[cc]);
-                    while (__any_sync(0xffffffffu, pend)) {
-                        pend = false;
-#pragma unroll
-                        for (int cc = 0; cc < CH; ++cc)
-                            if (tt[cc] >= 0 && is_pending(xv[cc])) {
-                                xv[cc] = ext[cc] ? ld_relaxed(out + jj[cc]) : xs[jj[cc] - c0];
-                                pend |= is_pending(xv[cc]);
-                            }
-                    }
-#pragma unroll
-                    for (int cc = 0; cc < CH; ++cc)
-#pragma unroll
-                        for (int t = 0; t < BS; ++t)
-                            if (tt[cc] == t) acc[t] = fma(v[cc], xv[cc], acc[t]);
-                }
-#pragma unroll
-                for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
-                if (active && gl == 0) {
-                    double xb[BS];
-                    const double* binv = rdiag;
-                    const double* bin = rdiag + BS;
-                    if (!UPPER) {
-                        int qq = 0;
-#pragma unroll
-                        for (int t = 0; t < BS; ++t) {
-                            double sacc = brhs[t] - acc[t];
-#pragma unroll
-                            for (int u = 0; u < t; ++u) sacc -= bin[qq++] * xb[u];
-                            xb[t] = sacc * binv[t];
-                        }
-                    } else {
-#pragma unroll
-                        for (int t = BS - 1; t >= 0; --t) {
-                            double sacc = brhs[t] - acc[t];
-                            int qq = 0;
-#pragma unroll
-                            for (int r = 0; r < t; ++r) qq += BS - 1 - r;
-#pragma unroll
-                            for (int u = t + 1; u < BS; ++u) sacc -= bin[qq + (u - t - 1)] * xb[u];
-                            xb[t] = sacc * binv[t];
-                        }
-                    }
-#pragma unroll
-                    for (int t = 0; t < BS; ++t) {
-                        xs[r0 + t - c0] = xb[t];
-                        st_relaxed(out + r0 + t, xb[t]);
-                    }
-                }
-                __syncwarp();
-                if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
-                if (lane == 0) mbar_arrive(empty + s);
-            }
-        }
-        q0 += static_cast<uint64_t>(ie - ib);
-        __syncthreads();
-    }
-}
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
-constexpr int kPrefetchWarps = 2;  // per CTA of the chunked sweep
-constexpr int kLead = 96;          // items prefetched ahead of the consumers
-
-// Chunked sync-free sweep.
-//
-// Persistent CTAs claim contiguous row chunks in sweep order (forward for
-// L, backward for U); a chunk's values live in shared memory while it is
-// being solved. Inside a chunk the warps take items of one chunk-local
-// level in order, so a dependency inside the chunk is a shared-memory
-// poll (~30 cycles) and only dependencies on earlier chunks go through L2.
-// On a natural-ordered mesh most of the critical path (the x- and y-chains)
-// then stays inside an SM. Deadlock-free: internal dependencies sit at
-// lower local levels (earlier items), external ones in chunks claimed
-// earlier by running CTAs.
-template <int LG, int BS, bool UPPER>
-__global__ void __launch_bounds__(512)
-chunk_trsv_kernel(int64_t nchunks, int64_t nb, int64_t cb, const int64_t* __restrict__ chunk_item_ptr,
-                  const int32_t* __restrict__ slots, const int64_t* __restrict__ rp,
-                  const int32_t* __restrict__ cols, const double* __restrict__ vals,
-                  const double* __restrict__ invd, const double* rhs, double* out, double* reset,
-                  const int* __restrict__ done, unsigned* counter, long long* trace) {
-    extern __shared__ double xs_raw[];
-    volatile double* xs = xs_raw;
-    __shared__ unsigned s_claim;
-    __shared__ unsigned s_done;  // items finished in the current chunk
-    volatile unsigned* s_done_v = &s_done;
-    if (done && *done) return;
-    constexpr int G = 32 / LG;
-    constexpr int CH = (LG >= 16) ? 4 : 2;
-    constexpr int NIB = BS * (BS - 1) / 2;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    const int grp = lane / LG, gl = lane % LG;
-    for (;;) {
-        if (threadIdx.x == 0) s_claim = atomicAdd(counter, 1u);
-        __syncthreads();
-        const unsigned claim = s_claim;
-        if (claim >= nchunks) return;
-        const int64_t c = UPPER ? nchunks - 1 - static_cast<int64_t>(claim) : static_cast<int64_t>(claim);
-        long long tc0 = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc0));
-        const int64_t b0 = c * cb, b1 = min(nb, b0 + cb);
-        const int64_t c0 = b0 * BS, c1 = b1 * BS;
-        for (int64_t i = threadIdx.x; i < c1 - c0; i += blockDim.x) xs[i] = pending_value();
-        if (threadIdx.x == 0) s_done = 0;
-        __syncthreads();
-        const int64_t ib = chunk_item_ptr[c], ie = chunk_item_ptr[c + 1];
-        if (warp < kPrefetchWarps) {
-            // prefetchers: pull the next items' slots, row pointers, entries,
-            // rhs and pivots into L1, at most kLead items ahead of the
-            // consumers, so a consumer's loads are L1 hits
-            const int pl = warp * 32 + lane;
-            for (int64_t k = ib + pl; k < ie; k += kPrefetchWarps * 32) {
-                while (k >= ib + *s_done_v + kLead) __nanosleep(64);
-                for (int g = 0; g < G; ++g) {
-                    const int32_t bk = __ldg(slots + k * G + g);
-                    if (bk < 0) continue;
-                    const int64_t rr = static_cast<int64_t>(bk) * BS;
-                    const int64_t e0 = __ldg(rp + rr), e1 = __ldg(rp + rr + BS);
-                    for (int64_t a = e0 & ~15LL; a < e1; a += 16) prefetch_l1(vals + a);
-                    for (int64_t a = e0 & ~31LL; a < e1; a += 32) prefetch_l1(cols + a);
-                    prefetch_l1(rhs + rr);
-                    prefetch_l1(invd + rr);
-                }
-            }
-        } else
-        for (int64_t it = ib + (warp - kPrefetchWarps); it < ie; it += nwarps - kPrefetchWarps) {
-            long long ti0 = 0, ti1 = 0;
-            if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ti0));
-            const int32_t blk = __ldg(slots + it * G + grp);
-            const bool active = blk >= 0;
-            const int64_t r0 = active ? static_cast<int64_t>(blk) * BS : c0;
-            int64_t rpv[BS + 1];
-#pragma unroll
-            for (int t = 0; t <= BS; ++t) rpv[t] = active ? __ldg(rp + r0 + t) : 0;
-            int64_t ob[BS], oc[BS];
-            int total = 0;
-#pragma unroll
-            for (int t = 0; t < BS; ++t) {
-                ob[t] = UPPER ? rpv[t] + (BS - t) : rpv[t];
-                oc[t] = active ? (UPPER ? rpv[t + 1] - ob[t] : rpv[t + 1] - (t + 1) - rpv[t]) : 0;
-                total += static_cast<int>(oc[t]);
-            }
-            double brhs[BS], binv[BS], bin[NIB > 0 ? NIB : 1];
-            if (active && gl == 0) {
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    brhs[t] = rhs[r0 + t];
-                    binv[t] = __ldg(invd + r0 + t);
-                }
-                int q = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int s = 0; s < BS; ++s) {
-                        if (!UPPER && s < t) bin[q++] = __ldg(vals + rpv[t + 1] - (t + 1) + s);
-                        if (UPPER && s > t) bin[q++] = __ldg(vals + rpv[t] + (s - t));
-                    }
-            }
-            double acc[BS];
-#pragma unroll
-            for (int t = 0; t < BS; ++t) acc[t] = 0.0;
-            const int tmax = __reduce_max_sync(0xffffffffu, total);
-            for (int base = 0; base < tmax; base += LG * CH) {
-                double v[CH], xv[CH];
-                int32_t jj[CH];
-                int tt[CH];
-                bool ext[CH];
-#pragma unroll
-                for (int cc = 0; cc < CH; ++cc) {
-                    int e = base + cc * LG + gl;
-                    tt[cc] = -1;
-                    jj[cc] = 0;
-                    v[cc] = 0.0;
-                    ext[cc] = false;
-                    if (e < total) {
-                        int t = 0;
-#pragma unroll
-                        for (int s = 0; s < BS - 1; ++s)
-                            if (t == s && e >= oc[s]) {
-                                e -= static_cast<int>(oc[s]);
-                                t = s + 1;
-                            }
-                        tt[cc] = t;
-                        jj[cc] = __ldg(cols + ob[t] + e);
-                        v[cc] = __ldg(vals + ob[t] + e);
-                        ext[cc] = UPPER ? jj[cc] >= c1 : jj[cc] < c0;
-                    }
-                }
-#pragma unroll
-                for (int cc = 0; cc < CH; ++cc)
-                    xv[cc] = tt[cc] < 0 ? 0.0 : (ext[cc] ? ld_relaxed(out + jj[cc]) : xs[jj[cc] - c0]);
-                bool pend = false;
-#pragma unroll
-                for (int cc = 0; cc < CH; ++cc) pend |= tt[cc] >= 0 && is_pending(xv[cc]);
-                while (__any_sync(0xffffffffu, pend)) {
-                    pend = false;
-#pragma unroll
-                    for (int cc = 0; cc < CH; ++cc)
-                        if (tt[cc] >= 0 && is_pending(xv[cc])) {
-                            xv[cc] = ext[cc] ? ld_relaxed(out + jj[cc]) : xs[jj[cc] - c0];
-                            pend |= is_pending(xv[cc]);
-                        }
-                }
-#pragma unroll
-                for (int cc = 0; cc < CH; ++cc)
-#pragma unroll
-                    for (int t = 0; t < BS; ++t)
-                        if (tt[cc] == t) acc[t] = fma(v[cc], xv[cc], acc[t]);
-            }
-            if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ti1));
-#pragma unroll
-            for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
-            if (active && gl == 0) {
-                double xb[BS];
-                if (!UPPER) {
-                    int q = 0;
-#pragma unroll
-                    for (int t = 0; t < BS; ++t) {
-                        double s = brhs[t] - acc[t];
-#pragma unroll
-                        for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                        xb[t] = s * binv[t];
-                    }
-                } else {
-#pragma unroll
-                    for (int t = BS - 1; t >= 0; --t) {
-                        double s = brhs[t] - acc[t];
-                        int q = 0;
-#pragma unroll
-                        for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                        for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                        xb[t] = s * binv[t];
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    xs[r0 + t - c0] = xb[t];
-                    st_relaxed(out + r0 + t, xb[t]);
-                }
-            }
-            __syncwarp();
-            if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
-            if (lane == 0) atomicAdd(&s_done, 1u);
-            if (trace && lane == 0) {
-                long long t2;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-                long long* tr = trace + 4 * nchunks + 4 * it;
-                tr[0] = ti0;
-                tr[1] = ti1;
-                tr[2] = t2;
-                tr[3] = warp;
-            }
-        }
-        __syncthreads();
-        if (trace && threadIdx.x == 0) {
-            long long tc1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc1));
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            trace[4 * c + 0] = tc0;
-            trace[4 * c + 1] = tc1;
-            trace[4 * c + 2] = smid;
-            trace[4 * c + 3] = claim;
-        }
-    }
 }
 
 }  // namespace pclab_b200
