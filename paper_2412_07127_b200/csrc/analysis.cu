@@ -296,30 +296,32 @@ __global__ void slots_fill(int64_t nitems, int per_item, const int32_t* __restri
     slots[k] = g < cnt[it] ? order[first[it] + g] : -1;
 }
 
-// Row pointers of every slot's block, stored with the schedule so an
-// item's first dependent load is its entries (node-blocked sweep): record
-// k = {rp[first row], row lengths packed 16 bits per row}.
+// Slot records (BsrSlot, 16 bytes): k = {block, rp[first row], bp[block],
+// row lengths packed 10 bits per row}, so an item's first dependent load is
+// its entries. Flags rows longer than 1023 entries or offsets beyond 32 bits.
 __global__ void slot_rp_fill(int64_t nslots, int bs, const int32_t* __restrict__ slots,
                              const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
-                             int64_t* __restrict__ srp, int* __restrict__ bad) {
+                             int32_t* __restrict__ srec, int* __restrict__ bad) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (k >= nslots) return;
     const int32_t b = slots[k];
-    int64_t r0 = 0;
-    unsigned long long lens = 0;
+    int64_t r0 = 0, c0 = 0;
+    uint32_t lens = 0;
     if (b >= 0) {
         const int64_t i = static_cast<int64_t>(b) * bs;
         r0 = rp[i];
-        for (int t = 0; t < bs; ++t) {
+        c0 = bp ? bp[b] : 0;
+        if (bs > 3 || r0 > 0xffffffffLL || c0 > 0xffffffffLL) *bad = 1;
+        for (int t = 0; t < bs && t < 3; ++t) {
             const int64_t len = rp[i + t + 1] - rp[i + t];
-            if (len > 0xffff) *bad = 1;
-            lens |= static_cast<unsigned long long>(len & 0xffff) << (16 * t);
+            if (len > 1023) *bad = 1;
+            lens |= static_cast<uint32_t>(len & 1023) << (10 * t);
         }
     }
-    srp[4 * k] = r0;
-    srp[4 * k + 1] = static_cast<int64_t>(lens);
-    srp[4 * k + 2] = b >= 0 && bp ? bp[b] : 0;
-    srp[4 * k + 3] = 0;
+    srec[4 * k] = b;
+    srec[4 * k + 1] = static_cast<int32_t>(static_cast<uint32_t>(r0));
+    srec[4 * k + 2] = static_cast<int32_t>(static_cast<uint32_t>(c0));
+    srec[4 * k + 3] = static_cast<int32_t>(lens);
 }
 
 // Block-column view (BlockCols). mode 0: L (off-block entries first),
@@ -350,6 +352,77 @@ __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* 
     for (int64_t p = s; p < e; p += per_item, ++it) {
         first[it] = p;
         cnt[it] = static_cast<int32_t>(min(static_cast<int64_t>(per_item), e - p));
+    }
+}
+
+// ---------------------------------------------------------------- tiles
+// Owner of block b: piece floor(b * P / nb) (contiguous ranges), piece k
+// runs on CTA k % C.
+__device__ __forceinline__ int64_t tile_owner(int64_t b, int64_t nb, int64_t P, int C) {
+    return (b * P / nb) % C;
+}
+
+__global__ void tile_keys(int64_t nb, int64_t P, int C, const int32_t* __restrict__ level,
+                          unsigned long long* __restrict__ key) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    key[b] = (static_cast<unsigned long long>(tile_owner(b, nb, P, C)) << 42) |
+             (static_cast<unsigned long long>(level[b]) << 22) | static_cast<unsigned long long>(b);
+}
+
+// run = one (owner, level) group of the sorted keys
+__global__ void tile_run_flags(int64_t nb, const unsigned long long* __restrict__ skey, int64_t* __restrict__ flag) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s >= nb) return;
+    flag[s] = (s == 0 || (skey[s] >> 22) != (skey[s - 1] >> 22)) ? 1 : 0;
+}
+
+__global__ void tile_run_first(int64_t nb, const int64_t* __restrict__ flag, const int64_t* __restrict__ runincl,
+                               int64_t* __restrict__ first) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s >= nb) return;
+    if (flag[s]) first[runincl[s] - 1] = s;
+    if (s == nb - 1) first[runincl[s]] = nb;
+}
+
+// padded run lengths (whole warp items of G blocks), in place of the next
+// run's first index shifted by one: len[r] for r < nruns, 0 at nruns
+__global__ void tile_run_len(int64_t nruns, int G, const int64_t* __restrict__ first, int64_t* __restrict__ plen) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r > nruns) return;
+    plen[r] = r < nruns ? (first[r + 1] - first[r] + G - 1) / G * G : 0;
+}
+
+__global__ void tile_place(int64_t nb, const unsigned long long* __restrict__ skey, const int64_t* __restrict__ runincl,
+                           const int64_t* __restrict__ first, const int64_t* __restrict__ rpos,
+                           int32_t* __restrict__ slots, int64_t* __restrict__ posof, int64_t* __restrict__ tbeg) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s >= nb) return;
+    const int64_t r = runincl[s] - 1;
+    const int64_t pos = rpos[r] + (s - first[r]);
+    const int64_t b = static_cast<int64_t>(skey[s] & ((1ULL << 22) - 1));
+    slots[pos] = static_cast<int32_t>(b);
+    posof[b] = pos;
+    const unsigned long long own = skey[s] >> 42;
+    if (s == 0 || own != (skey[s - 1] >> 42)) tbeg[own] = pos;
+}
+
+__global__ void tile_local(int64_t nb, int64_t P, int C, const int64_t* __restrict__ tbeg, int64_t* __restrict__ posof) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b < nb) posof[b] -= tbeg[tile_owner(b, nb, P, C)];
+}
+
+__global__ void tile_cols(int64_t nb, int bs, int64_t P, int C, const int64_t* __restrict__ bp,
+                          const int32_t* __restrict__ bcol, const int64_t* __restrict__ posof,
+                          uint32_t* __restrict__ tcol) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t ob = tile_owner(b, nb, P, C);
+    for (int64_t k = bp[b]; k < bp[b + 1]; ++k) {
+        const int64_t nbr = bcol[k] / bs;
+        int64_t d = tile_owner(nbr, nb, P, C) == ob ? posof[b] - posof[nbr] : 0;
+        if (d <= 0 || d >= (1 << kTileDistBits)) d = 0;
+        tcol[k] = (static_cast<uint32_t>(nbr) << kTileDistBits) | static_cast<uint32_t>(d);
     }
 }
 
@@ -490,6 +563,71 @@ static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, c
     }
 }
 
+
+// Tiled schedule of a node-blocked sweep (TileSched): `ntiles` CTAs,
+// `per_cta` contiguous pieces each. Needs < 2^22 blocks and < 2^20 levels
+// (key packing); returns false (no tile schedule) otherwise.
+static bool build_tiles(const DevCsr& M, const BlockCols& bc, Schedule& s, int ntiles, int per_cta,
+                        cudaStream_t st) {
+    TileSched& t = s.tile;
+    const int64_t nb = s.nblocks;
+    const int G = s.per_item;
+    if (nb == 0 || nb >= (1LL << 22) || s.nlevels >= (1 << 20)) return false;
+    const int C = static_cast<int>(std::min<int64_t>(ntiles, nb));
+    const int64_t P = std::min<int64_t>(static_cast<int64_t>(C) * std::max(per_cta, 1), nb);
+    t.ntiles = C;
+    t.pieces = P;
+    DevBuf<unsigned long long> key(nb), skey(nb);
+    tile_keys<<<grid_for(nb, 256), 256, 0, st>>>(nb, P, C, s.level.p, key.p);
+    CK_LAUNCH();
+    {
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tmp, key.p, skey.p, static_cast<int>(nb), 0, 64, st);
+        DevBuf<unsigned char> tb(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceRadixSort::SortKeys(tb.p, tmp, key.p, skey.p, static_cast<int>(nb), 0, 64, st);
+        CK(cudaStreamSynchronize(st));
+    }
+    DevBuf<int64_t> flag(nb), runincl(nb);
+    tile_run_flags<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, flag.p);
+    CK_LAUNCH();
+    {
+        size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, flag.p, runincl.p, nb, st);
+        DevBuf<unsigned char> tb(static_cast<int64_t>(tmp) + 1);
+        cub::DeviceScan::InclusiveSum(tb.p, tmp, flag.p, runincl.p, nb, st);
+    }
+    const int64_t nruns = dev_read(runincl.p + nb - 1, st);
+    DevBuf<int64_t> first(nruns + 1), rpos(nruns + 1);
+    tile_run_first<<<grid_for(nb, 256), 256, 0, st>>>(nb, flag.p, runincl.p, first.p);
+    CK_LAUNCH();
+    tile_run_len<<<grid_for(nruns + 1, 256), 256, 0, st>>>(nruns, G, first.p, rpos.p);
+    CK_LAUNCH();
+    scan_inplace(rpos.p, nruns + 1, st);
+    t.npos = dev_read(rpos.p + nruns, st);
+    t.slots.alloc(t.npos);
+    t.tbeg.alloc(C + 1);
+    CK(cudaMemsetAsync(t.slots.p, 0xff, sizeof(int32_t) * t.npos, st));
+    CK(cudaMemcpyAsync(t.tbeg.p + C, &t.npos, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    DevBuf<int64_t> posof(nb);
+    tile_place<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, runincl.p, first.p, rpos.p, t.slots.p, posof.p,
+                                                  t.tbeg.p);
+    CK_LAUNCH();
+    tile_local<<<grid_for(nb, 256), 256, 0, st>>>(nb, P, C, t.tbeg.p, posof.p);
+    CK_LAUNCH();
+    t.tcol.alloc(std::max<int64_t>(bc.bcol.n, 1));
+    tile_cols<<<grid_for(nb, 256), 256, 0, st>>>(nb, s.bs, P, C, bc.bp.p, bc.bcol.p, posof.p, t.tcol.p);
+    CK_LAUNCH();
+    DevBuf<int> bad(1);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    t.srp.alloc(4 * t.npos);
+    slot_rp_fill<<<grid_for(t.npos, 256), 256, 0, st>>>(t.npos, s.bs, t.slots.p, M.rp.p, bc.bp.p, t.srp.p, bad.p);
+    CK_LAUNCH();
+    if (dev_read(bad.p, st) != 0) {
+        t = TileSched{};
+        return false;
+    }
+    return true;
+}
 
 // ---------------------------------------------------------------- chains
 // Sweep-order index r of block b: lower sweeps run b = r, upper b = nb-1-r.
@@ -771,6 +909,21 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
                 CK_LAUNCH();
                 sc->need_crit = true;
             }
+        }
+    }
+    // tiled node-blocked sweeps (opt-in, PCLAB_TILE=1): one CTA per SM owns
+    // contiguous block ranges (PCLAB_TILE_K pieces per CTA, PCLAB_TILES
+    // CTAs). On configs[2] slower than the round-robin sweep (1.11 vs 1.03 ms
+    // at 32-64 pieces per CTA, 2.7 ms at 1): the shared-memory handoff saves
+    // little because the sweep is bound by its load stream, not the L2 hop
+    if (an->bsr) {
+        static const bool tile_on = getenv("PCLAB_TILE") && atoi(getenv("PCLAB_TILE")) != 0;
+        static const int tile_k = getenv("PCLAB_TILE_K") ? atoi(getenv("PCLAB_TILE_K")) : 1;
+        static const int tiles = getenv("PCLAB_TILES") ? atoi(getenv("PCLAB_TILES")) : 0;
+        if (tile_on) {
+            const int C = tiles > 0 ? std::min(tiles, sm_count()) : sm_count();
+            build_tiles(L, an->lbc, an->blk_lo, C, tile_k, st);
+            build_tiles(U, an->ubc, an->blk_up, C, tile_k, st);
         }
     }
     // node-blocked A: the PCG product reads one column index per block

@@ -56,6 +56,9 @@ int sm_count();
 // 32-bit fill writes it. Real results never carry this payload (arithmetic
 // NaNs are canonical 0x7ff8...).
 constexpr unsigned long long kPending = 0x7FFA5A5A7FFA5A5AULL;
+// Tiled sweep: bits of a packed block column that hold the distance back
+// to a same-CTA dependency (TileSched::tcol).
+constexpr int kTileDistBits = 10;
 // Row broke down during IC(0): dependants consume it and produce NaN.
 constexpr unsigned long long kBroken = 0x7FF8000000000000ULL;
 

@@ -64,6 +64,25 @@ struct DevCsr {
     DevBuf<double> vals;
 };
 
+// Tiled schedule of a node-blocked sweep (tile_trsv_kernel): the block
+// rows are cut into `pieces` contiguous ranges, piece k owned by CTA
+// k % ntiles. Each CTA runs its blocks in (level, index) order -- its list
+// is positions [tbeg[c], tbeg[c+1]), every level's run padded to whole
+// warp items -- and hands results to its own later blocks through a
+// shared-memory ring; only dependencies owned by another CTA go through
+// L2. Contiguous ranges make the cross-CTA dependencies one-directional.
+struct TileSched {
+    int ntiles = 0;
+    int64_t pieces = 0;
+    int64_t npos = 0;
+    DevBuf<int64_t> tbeg;   // [ntiles + 1] first position of each CTA's list
+    DevBuf<int32_t> slots;  // [npos] block at each position, -1 = padding
+    DevBuf<int32_t> srp;    // [4 * npos] slot records (as Schedule::slot_rp)
+    DevBuf<uint32_t> tcol;  // [block columns] (neighbour block << 10) | d, d = distance
+                            // back in the owner's list (1..1023) when the owner is
+                            // the same CTA, else 0 (read from L2)
+};
+
 // Dependency schedule of a triangular sweep over blocks of `bs`
 // consecutive rows: blocks sorted by (level, index) and cut into warp
 // items of at most `per_item` blocks of one level.
@@ -81,8 +100,8 @@ struct Schedule {
     DevBuf<int64_t> item_first;  // [nitems] first position in `order`
     DevBuf<int32_t> item_cnt;    // [nitems] blocks in the item
     DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
-    DevBuf<int64_t> slot_rp;     // [nitems * per_item * 4] {first row pointer, packed row lengths,
-                                 //  block-column offset, 0} of the slot's block (bsr)
+    DevBuf<int32_t> slot_rp;     // [nitems * per_item * 4] 16-byte slot records {block (-1 idle),
+                                 //  first row pointer, first block column, row lengths 10 bits each}
     // chain segments (node-blocked sweeps): runs of consecutive blocks where
     // each depends on the one before it in sweep order, cut at chain_k
     // blocks, sorted by (level of the first block, index), one per warp
@@ -94,6 +113,7 @@ struct Schedule {
     DevBuf<int32_t> seg_first;    // [chain_items] first block
     DevBuf<int32_t> seg_len;      // [chain_items]
     int64_t max_level_width = 0;
+    TileSched tile;               // built for node-blocked sweeps (tile_trsv_kernel)
 };
 
 // Block-column view of a node-blocked CSR matrix (Analysis::bsr): block

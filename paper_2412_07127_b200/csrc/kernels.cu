@@ -149,13 +149,14 @@ static long long* g_trace = nullptr;
 // idle pollers crowd L2.
 // Measured on configs[2]: 4 levels for the entry-lane sweep, 2 for the
 // node-blocked one (its pollers read BS values each, 1.40 vs 1.65 ms at 4).
-static unsigned trsv_grid(const Schedule& s, double depth_default) {
+static unsigned trsv_grid(const Schedule& s, double depth_default, int warps_per_cta = 8) {
     const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
     static const double env_depth = getenv("PCLAB_TRSV_DEPTH") ? atof(getenv("PCLAB_TRSV_DEPTH")) : 0.0;
     const double depth = env_depth > 0 ? env_depth : depth_default;
     const int64_t warps = static_cast<int64_t>(depth * per_level) + 1;
-    const int64_t blocks = (warps + 7) / 8;
-    return static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
+    const int64_t blocks = (warps + warps_per_cta - 1) / warps_per_cta;
+    return static_cast<unsigned>(
+        std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * (64 / warps_per_cta)));
 }
 
 template <int LG, int BS, bool UP>
@@ -204,10 +205,15 @@ static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr&
 template <int LG, int BS, bool UP>
 static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
                          const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
-    static const unsigned cap = resident_ctas(bsr_trsv_kernel<LG, BS, UP>);
-    const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
-    bsr_trsv_kernel<LG, BS, UP><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, bcol, vals, invd, b, x,
-                                                      reset, done, trsv_tune(), g_trace);
+    static unsigned cap = 0;
+    if (!cap) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP>, BSR_THREADS, 0));
+        cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+    }
+    const unsigned grid = std::min(trsv_grid(s, 3.0, BSR_THREADS / 32), cap);
+    bsr_trsv_kernel<LG, BS, UP><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b, x, reset,
+                                                              done, trsv_tune(), g_trace);
 }
 
 // CTAs given to the fused product (PCLAB_MV_CTAS overrides; default two per SM)
@@ -224,7 +230,7 @@ static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uv
     static const unsigned cap = resident_ctas(bsr_upper_mv_kernel<LG, BS>);
     const unsigned nsweep = std::min(trsv_grid(s, 2.0), cap);
     bsr_upper_mv_kernel<LG, BS><<<nsweep + mv_ctas(), 256, 0, st>>>(
-        s.nitems, s.slots.p, s.slot_rp.p, an.ubc.bcol.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
+        s.nitems, s.slot_rp.p, an.ubc.bcol.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
         an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
 }
 
@@ -233,8 +239,36 @@ static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, 
                         double* x, double* reset, const int* done, cudaStream_t st) {
     static const unsigned cap = resident_ctas(rr_trsv_kernel<LG, BS, UP, CH>);
     const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
-    rr_trsv_kernel<LG, BS, UP, CH><<<grid, 256, 0, st>>>(s.nitems, s.slots.p, s.slot_rp.p, M.cols.p, vals, invd, b,
+    rr_trsv_kernel<LG, BS, UP, CH><<<grid, 256, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals, invd, b,
                                                           x, reset, done, trsv_tune());
+}
+
+// Tiled sweep: one 512-thread CTA per tile, all resident (1 per SM).
+// PCLAB_TILE_RING=64 selects a 64-slot ring (test knob: dependencies up to
+// 1023 positions back then often find their slot recycled and take the L2
+// path).
+constexpr int kTileRing = 2048;  // ring slots (64 KB of shared memory)
+
+template <int LG, int BS, bool UP, int RING>
+static void launch_tile_r(const TileSched& t, const double* vals, const double* invd, const double* b, double* x,
+                          double* reset, const int* done, cudaStream_t st) {
+    constexpr size_t smem = sizeof(TileSlot) * RING;
+    static bool set = false;
+    if (!set) {
+        CK(cudaFuncSetAttribute(tile_trsv_kernel<LG, BS, UP, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        set = true;
+    }
+    tile_trsv_kernel<LG, BS, UP, RING><<<t.ntiles, 512, smem, st>>>(t.tbeg.p, t.srp.p, t.tcol.p, vals,
+                                                                     invd, b, x, reset, done);
+}
+
+template <int LG, int BS, bool UP>
+static void launch_tile_t(const Schedule& s, const double* vals, const double* invd, const double* b, double* x,
+                          double* reset, const int* done, cudaStream_t st) {
+    static const bool small = getenv("PCLAB_TILE_RING") && atoi(getenv("PCLAB_TILE_RING")) == 64;
+    if (small) launch_tile_r<LG, BS, UP, 64>(s.tile, vals, invd, b, x, reset, done, st);
+    else launch_tile_r<LG, BS, UP, kTileRing>(s.tile, vals, invd, b, x, reset, done, st);
 }
 
 template <int BS, bool UP>
@@ -244,6 +278,16 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
     if constexpr (BS > 1) {
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
+            if (s.tile.ntiles > 0) {
+                switch (s.lanes) {
+                    case 2:
+                    case 4: launch_tile_t<4, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
+                    case 8: launch_tile_t<8, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
+                    case 16: launch_tile_t<16, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
+                    default: launch_tile_t<32, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
+                }
+                return;
+            }
             bool chained = false;
             chained = launch_chain_t<BS, UP>(s, *bc, M, vals, invd, b, x, reset, done, st);
             if (chained) return;

@@ -13,6 +13,14 @@
 #ifndef BSR_MINB
 #define BSR_MINB 2
 #endif
+// node-blocked sweep CTA: 128 threads, 5 resident per SM (20 warps within
+// the register file at <= 102 registers per thread)
+#ifndef BSR_THREADS
+#define BSR_THREADS 128
+#endif
+#ifndef BSR_CTAS
+#define BSR_CTAS 5
+#endif
 
 namespace pclab_b200 {
 
@@ -336,34 +344,58 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
     }
 }
 
-// Per-item state of the node-blocked sweep: the slot's block, its first
-// row pointer and packed row lengths (Schedule::slot_rp), and -- for the
-// next two items -- the right-hand side.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte asynchronous global -> shared copy (LDGSTS), evict-first in L2
+// like ld_stream: the matrix stream is read once per sweep.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n\t}" ::"r"(smem_addr(dst)),
+        "l"(src)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// doubles of one block's staged rows (node-blocked sweep): 3 elasticity
+// rows of <= 42 entries, 16-byte aligned
+constexpr int kStageD = 128;
+constexpr int kStages = 3;
+
+// Per-item state of the node-blocked sweep: one 16-byte slot record
+// (Schedule::slot_rp) = {block (-1: idle lane group), first row pointer,
+// first block column, the BS row lengths packed 10 bits each}.
 struct BsrSlot {
-    int32_t blk;  // -1: idle lane group
-    int64_t r0;
-    unsigned long long lens;
-    int64_t bp;   // first block column of the block row
+    int32_t blk;
+    uint32_t r0;
+    uint32_t bp;
+    uint32_t lens;
 };
 
 __device__ __forceinline__ BsrSlot bsr_slot(int64_t it, int64_t nitems, int G, int grp,
-                                            const int32_t* __restrict__ slots, const int64_t* __restrict__ srp) {
-    BsrSlot m;
-    const bool ok = it < nitems;
-    const int64_t k = it * G + grp;
-    m.blk = ok ? __ldg(slots + k) : -1;
-    const longlong2 v = ok ? __ldg(reinterpret_cast<const longlong2*>(srp) + 2 * k) : make_longlong2(0, 0);
-    m.r0 = v.x;
-    m.lens = static_cast<unsigned long long>(v.y);
-    m.bp = ok ? __ldg(srp + 4 * k + 2) : 0;
-    return m;
+                                            const int32_t* __restrict__ srec) {
+    const int4 v = it < nitems ? __ldg(reinterpret_cast<const int4*>(srec) + (it * G + grp)) : make_int4(-1, 0, 0, 0);
+    return BsrSlot{v.x, static_cast<uint32_t>(v.y), static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
 }
 
 template <int BS>
 __device__ __forceinline__ void slot_rows(const BsrSlot& m, int64_t (&rp)[BS + 1]) {
     rp[0] = m.r0;
 #pragma unroll
-    for (int t = 0; t < BS; ++t) rp[t + 1] = rp[t] + static_cast<int64_t>((m.lens >> (16 * t)) & 0xffff);
+    for (int t = 0; t < BS; ++t) rp[t + 1] = rp[t] + static_cast<int64_t>((m.lens >> (10 * t)) & 1023u);
+}
+
+// Neighbour blocks of a slot's block (node-blocked sweeps): row 0 holds
+// them all plus the diagonal (L) or the whole diagonal block row (U).
+template <int BS, bool UPPER>
+__device__ __forceinline__ int slot_nb(const BsrSlot& m) {
+    if (m.blk < 0) return 0;
+    const int len0 = static_cast<int>(m.lens & 1023u);
+    return (len0 - (UPPER ? BS : 1)) / BS;
 }
 
 // Node-blocked sweep (Analysis::bsr: the off-block pattern is made of
@@ -383,20 +415,24 @@ __device__ __forceinline__ void slot_rows(const BsrSlot& m, int64_t (&rp)[BS + 1
 //   item k+3: slot record        item k+2: entries prefetched into L1
 //   item k+1: right-hand side    item k:   entries, dependency polls
 template <int LG, int BS, bool UPPER>
-__device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ slots,
-                                          const int64_t* __restrict__ srp, const int32_t* __restrict__ bcol,
+__device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ srec, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
                                           const double* rhs, double* out, double* reset, int64_t warp,
-                                          int64_t nwarps, unsigned sleep_ns, long long* trace) {
+                                          int64_t nwarps, int tune, long long* trace) {
+    // tune: sleep_ns << 8 | experiment bits (developer timing probes that
+    // give WRONG results: 1 = matrix values from one cached line, 2 = no
+    // dependency waits)
+    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+    const bool exp_vals = tune & 1, exp_nowait = tune & 2;
     constexpr int G = 32 / LG;
     constexpr int NIB = BS * (BS - 1) / 2;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     int64_t it = warp;
-    BsrSlot m = bsr_slot(it, nitems, G, grp, slots, srp);
-    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, slots, srp);
-    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, slots, srp);
-    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
+    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
+    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
     double rhs0[BS], rhs1[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
@@ -459,9 +495,13 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
 #pragma unroll
                 for (int t = 0; t < BS; ++t)
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) a[t][c] = ld_stream(vals + ob[t] + BS * n + c);
+                    for (int c = 0; c < BS; ++c)
+                        a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
 #pragma unroll
                 for (int c = 0; c < BS; ++c) xv[c] = ld_relaxed(out + xc + c);
+                if (exp_nowait)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
             } else {
 #pragma unroll
                 for (int t = 0; t < BS; ++t) {
@@ -533,7 +573,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         m = m1;
         m1 = m2;
         m2 = m3;
-        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
 #pragma unroll
         for (int t = 0; t < BS; ++t) {
             rhs0[t] = rhs1[t];
@@ -543,16 +583,240 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
 }
 
 template <int LG, int BS, bool UPPER>
-__global__ void __launch_bounds__(256, BSR_MINB)
-bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+__global__ void __launch_bounds__(BSR_THREADS, BSR_CTAS)
+bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                 const double* __restrict__ invd, const double* rhs, double* out, double* reset,
                 const int* __restrict__ done, int tune, long long* trace) {
     if (done && *done) return;
-    bsr_sweep<LG, BS, UPPER>(nitems, slots, srp, bcol, vals, invd, rhs, out, reset,
+    bsr_sweep<LG, BS, UPPER>(nitems, srec, bcol, vals, invd, rhs, out, reset,
                              (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
-                             (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, static_cast<unsigned>(tune >> 8),
-                             trace);
+                             (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, tune, trace);
+}
+
+// ------------------------------------------------------------------------
+// Tiled node-blocked sweep (TileSched). CTA c owns contiguous ranges of
+// block rows and runs them in (level, index) order, items dealt round-robin
+// to its warps exactly like bsr_sweep. A block's result goes to L2 (for the
+// other CTAs and the caller) and into a shared-memory ring slot indexed by
+// its list position, so a dependency owned by the same CTA -- most of them
+// for a contiguous range -- is read from shared memory (~tens of ns) instead
+// of a round trip through L2 (~1 us under the sweep's load). The slot is a
+// seqlock: {tag, values}; the writer sets tag = -1, fences, writes the
+// values, fences, sets tag = position. A reader accepts the values when the
+// tag equals the dependency's position before and after reading them; a tag
+// beyond it means the slot was recycled and the value is read from L2.
+struct __align__(16) TileSlot {
+    int tag;
+    int pad;
+    double v[3];
+};
+
+__device__ __forceinline__ int lds_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+template <int LG, int BS, bool UPPER, int RING>
+__global__ void __launch_bounds__(512, 1)
+tile_trsv_kernel(const int64_t* __restrict__ tbeg, const int32_t* __restrict__ tsrec,
+                 const uint32_t* __restrict__ tcol,
+                 const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs, double* out,
+                 double* reset, const int* __restrict__ done) {
+    static_assert(BS <= 3, "ring slots hold 3 values");
+    extern __shared__ __align__(16) unsigned char tile_smem[];
+    TileSlot* ring = reinterpret_cast<TileSlot*>(tile_smem);
+    if (done && *done) return;
+    for (int i = threadIdx.x; i < RING; i += blockDim.x) ring[i].tag = -1;
+    __syncthreads();
+    constexpr int G = 32 / LG;
+    constexpr int NIB = BS * (BS - 1) / 2;
+    constexpr uint32_t DMASK = (1u << kTileDistBits) - 1;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    const int64_t base = tbeg[blockIdx.x];
+    const int64_t nitems = (tbeg[blockIdx.x + 1] - base) / G;
+    const int32_t* srec = tsrec + 4 * base;
+    const int64_t nwarps = blockDim.x >> 5;
+    int64_t it = threadIdx.x >> 5;
+    BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
+    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
+    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+    double rhs0[BS], rhs1[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) {
+        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
+        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+    }
+    auto prefetch = [&](const BsrSlot& q) {
+        if (q.blk >= 0) {
+            int64_t rq[BS + 1];
+            slot_rows<BS>(q, rq);
+            const int64_t e0 = rq[0], e1 = rq[BS];
+            for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
+            if (gl == 0) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(tcol + q.bp));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + static_cast<int64_t>(q.blk) * BS));
+            }
+        }
+    };
+    auto first_code = [&](const BsrSlot& q) {
+        return gl < slot_nb<BS, UPPER>(q) ? ld_stream(reinterpret_cast<const int32_t*>(tcol) + q.bp + gl) : 0;
+    };
+    prefetch(m);
+    prefetch(m1);
+    int32_t code0 = first_code(m), code1 = first_code(m1);
+    while (it < nitems) {
+        prefetch(m2);
+        const bool active = m.blk >= 0;
+        const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
+        const int pos = static_cast<int>(it * G + grp);  // position in this CTA's list
+        int64_t mrp[BS + 1];
+        slot_rows<BS>(m, mrp);
+        int64_t ob[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
+        const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
+        double binv[BS], bin[NIB > 0 ? NIB : 1];
+        if (active && gl == 0) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
+            int q = 0;
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int s = 0; s < BS; ++s) {
+                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
+                    if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
+                }
+        }
+        double acc[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
+        for (int n0 = 0; n0 < nbmax; n0 += LG) {
+            const int n = n0 + gl;
+            const bool own = n < nb;
+            double a[BS][BS], xv[BS];
+            int64_t xc = 0;
+            int target = -1;  // >= 0: read the ring slot of this position
+            bool need = false;
+#pragma unroll
+            for (int t = 0; t < BS; ++t) xv[t] = 0.0;
+            if (own) {
+                const uint32_t code = static_cast<uint32_t>(
+                    n0 == 0 ? code0 : ld_stream(reinterpret_cast<const int32_t*>(tcol) + m.bp + n));
+                xc = static_cast<int64_t>(code >> kTileDistBits) * BS;
+                const int d = static_cast<int>(code & DMASK);
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) a[t][c] = ld_stream(vals + ob[t] + BS * n + c);
+                if (d) {
+                    target = pos - d;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) xv[c] = ld_relaxed(out + xc + c);
+                }
+                need = true;
+            } else {
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
+            }
+            while (__any_sync(0xffffffffu, need)) {
+                if (need) {
+                    if (target >= 0) {
+                        TileSlot* sl = ring + (target & (RING - 1));
+                        const int t1 = lds_volatile(&sl->tag);
+                        if (t1 == target) {
+                            __threadfence_block();
+                            double w[BS];
+#pragma unroll
+                            for (int c = 0; c < BS; ++c) w[c] = *reinterpret_cast<volatile double*>(&sl->v[c]);
+                            __threadfence_block();
+                            const int t2 = lds_volatile(&sl->tag);
+                            if (t2 == target) {
+#pragma unroll
+                                for (int c = 0; c < BS; ++c) xv[c] = w[c];
+                                need = false;
+                            } else if (t2 > target) {
+                                target = -1;  // recycled: the value is in L2
+#pragma unroll
+                                for (int c = 0; c < BS; ++c) xv[c] = pending_value();
+                            }
+                        } else if (t1 > target) {
+                            target = -1;
+#pragma unroll
+                            for (int c = 0; c < BS; ++c) xv[c] = pending_value();
+                        }
+                    } else {
+                        bool pend = false;
+#pragma unroll
+                        for (int c = 0; c < BS; ++c)
+                            if (is_pending(xv[c])) {
+                                xv[c] = ld_relaxed(out + xc + c);
+                                pend |= is_pending(xv[c]);
+                            }
+                        need = pend;
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+        if (active && gl == 0) {
+            double xb[BS];
+            if (!UPPER) {
+                int q = 0;
+#pragma unroll
+                for (int t = 0; t < BS; ++t) {
+                    double s = rhs0[t] - acc[t];
+#pragma unroll
+                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            } else {
+#pragma unroll
+                for (int t = BS - 1; t >= 0; --t) {
+                    double s = rhs0[t] - acc[t];
+                    int q = 0;
+#pragma unroll
+                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
+#pragma unroll
+                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
+                    xb[t] = s * binv[t];
+                }
+            }
+            TileSlot* sl = ring + (pos & (RING - 1));
+            *reinterpret_cast<volatile int*>(&sl->tag) = -1;
+            __threadfence_block();
+#pragma unroll
+            for (int t = 0; t < BS; ++t) *reinterpret_cast<volatile double*>(&sl->v[t]) = xb[t];
+            __threadfence_block();
+            *reinterpret_cast<volatile int*>(&sl->tag) = pos;
+#pragma unroll
+            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+        }
+        __syncwarp();
+        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+        it += nwarps;
+        m = m1;
+        m1 = m2;
+        m2 = m3;
+        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+        code0 = code1;
+        code1 = first_code(m1);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            rhs0[t] = rhs1[t];
+            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+        }
+    }
 }
 
 // Round-robin sweep for matrices that are not node-blocked (Poisson, FV
@@ -563,7 +827,7 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t
 // block's rows in order) instead of over neighbour blocks.
 template <int LG, int BS, bool UPPER, int CH>
 __global__ void __launch_bounds__(256, BSR_MINB)
-rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                const int32_t* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ invd,
                const double* rhs, double* out, double* reset, const int* __restrict__ done, int tune) {
     if (done && *done) return;
@@ -574,10 +838,10 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t*
     const int grp = lane / LG, gl = lane % LG;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     int64_t it = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    BsrSlot m = bsr_slot(it, nitems, G, grp, slots, srp);
-    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, slots, srp);
-    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, slots, srp);
-    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+    BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
+    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
+    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
     double rhs0[BS], rhs1[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
@@ -711,7 +975,7 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t*
         m = m1;
         m1 = m2;
         m2 = m3;
-        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, slots, srp);
+        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
 #pragma unroll
         for (int t = 0; t < BS; ++t) {
             rhs0[t] = rhs1[t];
@@ -840,7 +1104,7 @@ __device__ __forceinline__ void bsr_mv(int64_t nb, const int32_t* __restrict__ o
 // wait on sweep items, and the sweep CTAs are the first ones resident.
 template <int LG, int BS>
 __global__ void __launch_bounds__(256, BSR_MINB)
-bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int64_t* __restrict__ srp,
+bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                     const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                     const double* __restrict__ invd, const double* rhs, double* out, double* reset,
                     unsigned nsweep, int64_t nb, const int32_t* __restrict__ order,
@@ -852,19 +1116,15 @@ bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int
     if (threadIdx.x == 0) role = atomicAdd(counters + 1, 1u);
     __syncthreads();
     if (role < nsweep)
-        bsr_sweep<LG, BS, true>(nitems, slots, srp, bcol, vals, invd, rhs, out, reset,
+        bsr_sweep<LG, BS, true>(nitems, srec, bcol, vals, invd, rhs, out, reset,
                                 static_cast<int64_t>(role) * (blockDim.x >> 5) + (threadIdx.x >> 5),
-                                static_cast<int64_t>(nsweep) * (blockDim.x >> 5), static_cast<unsigned>(tune >> 8),
-                                trace);
+                                static_cast<int64_t>(nsweep) * (blockDim.x >> 5), tune & ~0xff, trace);
     else
         bsr_mv<BS>(nb, order, arp, acols, avals, out, w, counters + 2);
 }
 
 // ------------------------------------------------------------------------
 // mbarrier / bulk-copy helpers (chain.cuh)
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
