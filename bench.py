@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--kind", default="ic0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=2, help="PCG iterations per reference step")
+    ap.add_argument("--bw-sweep", action="store_true",
+                    help="BASELINE configs[4]: per-kernel bandwidth of SpMV / both sweeps at 64^3, 128^3, "
+                         "256^3 and the IC(0)+GNN PCG solve at each size (one JSON line per size)")
     return ap.parse_args()
 
 
@@ -50,6 +53,18 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d[workload][kernel.split(" ")[0]]
+        return e["dram_bytes"]
+    except Exception:
+        return None
 
 
 class Clocks:
@@ -223,61 +238,27 @@ def run_b200(args, w):
     ms, cg, its_all = combine_ranks(ms, cg, its, world, "cuda")
     value = its_all / cg
 
-    # per-kernel device times of the loop (eager iterations, events between kernels)
+    # per-kernel device times of the loop (eager iterations, events between
+    # kernels) and their algorithmic bytes (paper_2412_07127_b200/traffic.py)
+    from paper_2412_07127_b200 import traffic as T
     prof = pc.profile_device(bt.data_ptr(), xt.data_ptr(), 20)
     info = pc.info()
     hbm, peak_kind = peaks()
-    nl = info["nnz_lower"]
     lay = pc.layout()
-    # algorithmic HBM bytes per launch of each kernel, for the layout it runs on
-    if lay["node_blocked"]:
-        # node-blocked sweep: L values once, one column index per 3x3 block,
-        # the slot schedule (4-byte slot + 32-byte row record), rhs, 1/l_ii,
-        # solution write and the re-arm write of the other sweep vector
-        def sweep_bytes_of(bc, slots):
-            return 8 * nl + 4 * bc + 36 * slots + 4 * 8 * n
-        sweep_lo = sweep_bytes_of(lay["block_cols_lower"], lay["slots_lower"])
-        sweep_up = sweep_bytes_of(lay["block_cols_upper"], lay["slots_upper"])
-        sweep_name = "bsr_trsv_kernel (node-blocked sweep)"
-    else:
-        sweep_lo = sweep_up = 12 * nl + 8 * (n + 1) + 4 * 8 * n  # L vals+cols, row_ptr, rhs, x, 1/l_ii, reset
-        sweep_name = "trsv_kernel (lower sweep)"
-    if lay["a_node_blocked"]:
-        # p <- z + beta p (24n) then q = A p: A values, block columns, row and
-        # block pointers, p gathered once, q written
-        spmv_bytes = 24 * n + 8 * nnz + 4 * lay["block_cols_a"] + 8 * n + 8 * (n // 3 + 1) + 2 * 8 * n
-    else:
-        spmv_bytes = 24 * n + 12 * nnz + 8 * (n + 1) + 2 * 8 * n
-    # reference format (scalar CSR, int32 columns): two sweeps, p update +
-    # product, axpy + norm, dot
-    csr_bytes = (2 * (12 * nl + 8 * (n + 1) + 4 * 8 * n) + (24 * n + 12 * nnz + 8 * (n + 1) + 2 * 8 * n)
-                 + 6 * 8 * n + 2 * 8 * n)
+    kern = T.iteration_kernels(pc, n, nnz, prof)
     if prof["fused"]:
-        fused_bytes = sweep_up + spmv_bytes - 24 * n
-        kern = {
-            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": sweep_lo},
-            "sweep_upper_spmv": {"ms": prof["sweep_upper_ms"], "bytes": fused_bytes},
-            "pq_update": {"ms": prof["spmv_ms"], "bytes": 6 * 8 * n},
-            "axpy_norm": {"ms": prof["axpy_ms"], "bytes": 6 * 8 * n},
-            "dot": {"ms": prof["dot_ms"], "bytes": 2 * 8 * n},
-        }
         top, top_name = "sweep_upper_spmv", "bsr_upper_mv_kernel (fused sweep + product)"
+    elif lay["node_blocked"]:
+        top, top_name = "sweep_lower", "bsr_trsv_kernel (node-blocked sweep)"
     else:
-        kern = {
-            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": sweep_lo},
-            "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": sweep_up},
-            "spmv_p": {"ms": prof["spmv_ms"], "bytes": spmv_bytes},
-            "axpy_norm": {"ms": prof["axpy_ms"], "bytes": 6 * 8 * n},
-            "dot": {"ms": prof["dot_ms"], "bytes": 2 * 8 * n},
-        }
-        top, top_name = "sweep_lower", sweep_name
-    for k in kern.values():
-        k["gbs"] = k["bytes"] / k["ms"] / 1e6
+        top, top_name = "sweep_lower", "rr_trsv_kernel (lower sweep)"
+    csr_bytes = T.csr_iteration_bytes(nnz, info["nnz_lower"], n)
     iter_bytes = sum(k["bytes"] for k in kern.values())
     iter_ms = sum(k["ms"] for k in kern.values())
     achieved = kern[top]["gbs"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": top_name,
+                "frac": achieved / hbm, "traffic": ncu_traffic(w.name, top_name),
+                "kernel": top_name,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "iteration": {"bytes": iter_bytes, "ms": iter_ms, "gbs": iter_bytes / iter_ms / 1e6,
                               "frac": iter_bytes / iter_ms / 1e6 / hbm,
@@ -349,8 +330,80 @@ def run_b200(args, w):
         dist.destroy_process_group()
 
 
+def run_bw_sweep(args):
+    """configs[4] family (7-point FV diffusion, k = 10^u, u ~ U[-3,3]): each
+    kernel timed alone with CUDA events around every launch and L2 flushed
+    (a 512 MB write) before each, so the 64^3 / 128^3 systems that fit in
+    L2 are measured from HBM; then gnnic PCG to rel 1e-8 (max 5000)."""
+    import torch
+    import paper_2412_07127_b200 as P
+    from paper_2412_07127_b200 import traffic as T
+    import paper_2412_07127_b200.workloads as WL
+
+    torch.cuda.set_device(0)
+    hbm, peak_kind = peaks()
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    base = WL.by_name("diffusion_fv_256")
+    for m in (64, 128, 256):
+        w = base if m == 256 else base.scaled(m)
+        a, b_host, model = WL.build(w)
+        n, _, nnz = a.shape()
+        pc = P.Precond(a, "gnnic", model)
+        lay, info = pc.layout(), pc.info()
+        x = torch.randn(n, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+
+        def timed(f, reps=10):
+            ts = []
+            for _ in range(reps + 2):
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                f()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return float(np.median(ts[2:]))
+
+        bs = max(info["block_size"], 1)
+        ks = {
+            "spmv": (timed(lambda: a.spmv_device(x.data_ptr(), y.data_ptr())), T.spmv_bytes(lay, nnz, n, bs)),
+            "sweep_lower": (timed(lambda: pc.trsv_device(False, x.data_ptr(), y.data_ptr())),
+                            T.sweep_bytes(lay, info["nnz_lower"], n, False)),
+            "sweep_upper": (timed(lambda: pc.trsv_device(True, x.data_ptr(), y.data_ptr())),
+                            T.sweep_bytes(lay, info["nnz_lower"], n, True)),
+        }
+        kern = {k: {"ms": v[0], "bytes": v[1], "gbs": v[1] / v[0] / 1e6, "frac": v[1] / v[0] / 1e6 / hbm}
+                for k, v in ks.items()}
+        bt = torch.from_numpy(b_host).cuda()
+        xt = torch.zeros_like(bt)
+        pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=w.rel_tol, max_iters=w.max_iters)  # warm
+        xt.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a.drop_analysis()
+        pc2 = P.Precond(a, "gnnic", model)
+        rep = pc2.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=w.rel_tol, max_iters=w.max_iters)
+        torch.cuda.synchronize()
+        ttt = time.perf_counter() - t0
+        print(json.dumps({
+            "metric": "kernel_bandwidth_sweep", "workload": w.name, "m": m, "n": n, "nnz": nnz,
+            "kind": "gnnic", "levels": [info["block_levels_lower"], info["block_levels_upper"]],
+            "peak_gbs": hbm, "peak_source": peak_kind, "l2": "flushed before every launch",
+            "kernels": kern,
+            "pcg": {"iterations": rep["iterations"], "converged": rep["converged"],
+                    "time_to_tol_s": ttt, "cg_s": rep["cg_time"],
+                    "iters_per_s": rep["iterations"] / rep["cg_time"] if rep["cg_time"] else None,
+                    "true_rel_residual": rep["true_rel_residual"]},
+        }), flush=True)
+        del pc, pc2, a
+
+
 def main():
     args = parse()
+    if args.bw_sweep:
+        run_bw_sweep(args)
+        return
     import paper_2412_07127_b200.workloads as WL
     w = WL.by_name(args.config)
     if w is None:

@@ -1,0 +1,70 @@
+"""Algorithmic HBM bytes of the PCG-loop kernels (the roofline numerators).
+
+Per launch, for the layout the kernels actually run on (Precond.layout()):
+
+* node-blocked sweep (bsr_trsv_kernel): every factor value once (8 B), one
+  column index per 3x3 block (4 B), one 16-byte slot record per slot, and
+  per row the right-hand side, 1/l_ii, the solution write and the re-arm
+  write of the other sweep vector (4 x 8 B);
+* entry-lane sweep (rr_trsv_kernel, not node-blocked): value + column index
+  per entry (12 B), the slot records, the same 32 B per row;
+* product (k_pupdate + k_spmv_bsr_pap / k_spmv_pap): p <- z + beta p
+  (24 B/row), A's values (8 B) + block or entry column indices, row / block
+  pointers, p gathered once, q written;
+* axpy (x += alpha p, r -= alpha q, ||r||): 48 B/row; dot (r.z): 16 B/row.
+
+The reference's own format (scalar CSR, int32 columns, int64 row pointers)
+is reported beside it as `csr_equivalent_bytes`.
+"""
+from __future__ import annotations
+
+
+def sweep_bytes(lay: dict, nnz_lower: int, n: int, upper: bool) -> int:
+    slots = lay["slots_upper" if upper else "slots_lower"]
+    if lay["node_blocked"]:
+        bc = lay["block_cols_upper" if upper else "block_cols_lower"]
+        return 8 * nnz_lower + 4 * bc + 16 * slots + 32 * n
+    return 12 * nnz_lower + 16 * slots + 32 * n
+
+
+def product_bytes(lay: dict, nnz: int, n: int, bs: int) -> int:
+    if lay["a_node_blocked"]:
+        return 24 * n + 8 * nnz + 4 * lay["block_cols_a"] + 8 * n + 8 * (n // bs + 1) + 16 * n
+    return 24 * n + 12 * nnz + 8 * (n + 1) + 16 * n
+
+
+def spmv_bytes(lay: dict, nnz: int, n: int, bs: int) -> int:
+    """Stand-alone y = A x (no p update)."""
+    return product_bytes(lay, nnz, n, bs) - 24 * n
+
+
+def csr_iteration_bytes(nnz: int, nnz_lower: int, n: int) -> int:
+    sweep = 12 * nnz_lower + 8 * (n + 1) + 32 * n
+    return 2 * sweep + (24 * n + 12 * nnz + 8 * (n + 1) + 16 * n) + 48 * n + 16 * n
+
+
+def iteration_kernels(pc, n: int, nnz: int, prof: dict) -> dict:
+    """{kernel: {ms, bytes, gbs}} for one PCG iteration from a
+    Precond.profile_device() result."""
+    lay = pc.layout()
+    info = pc.info()
+    nl, bs = info["nnz_lower"], max(info["block_size"], 1)
+    lo, up = sweep_bytes(lay, nl, n, False), sweep_bytes(lay, nl, n, True)
+    prod = product_bytes(lay, nnz, n, bs)
+    if prof.get("fused"):
+        kern = {
+            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
+            "sweep_upper_spmv": {"ms": prof["sweep_upper_ms"], "bytes": up + prod - 24 * n},
+            "pq_update": {"ms": prof["spmv_ms"], "bytes": 48 * n},
+        }
+    else:
+        kern = {
+            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
+            "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": up},
+            "spmv_p": {"ms": prof["spmv_ms"], "bytes": prod},
+        }
+    kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": 48 * n}
+    kern["dot"] = {"ms": prof["dot_ms"], "bytes": 16 * n}
+    for k in kern.values():
+        k["gbs"] = k["bytes"] / k["ms"] / 1e6 if k["ms"] > 0 else None
+    return kern
