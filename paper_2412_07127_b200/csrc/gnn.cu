@@ -19,54 +19,44 @@ namespace {
 constexpr int kF = 9, kH = 8;
 __constant__ double c_p[997];
 
-struct MlpOff {
-    int w1, b1, w2, b2, in, out;
-};
-// ParamLayout (src/gnn.cpp:14-41)
-struct Layout {
-    MlpOff edge[3], node[3];
-};
-Layout make_layout() {
-    Layout L{};
+// ParamLayout (src/gnn.cpp:14-41) as compile-time offsets: block b holds
+// the edge MLP (in -> kH -> 1) then the node MLP (in -> kH -> kH), each as
+// W1 [kH x in], b1 [kH], W2 [out x kH], b2 [out], after 18 leading entries.
+// With constant offsets every weight is a direct constant-bank operand of
+// its FMA (no address arithmetic, no LDC per weight).
+constexpr int edge_in(int b) { return b == 0 ? 1 + 2 * kF : 2 + 2 * kH; }
+constexpr int node_in(int b) { return b == 0 ? kF + 2 : kH + 2; }
+constexpr int mlp_size(int in, int out) { return kH * in + kH + out * kH + out; }
+constexpr int edge_off(int b) {
     int off = 18;
-    const int ein[3] = {1 + 2 * kF, 2 + 2 * kH, 2 + 2 * kH};
-    const int nin[3] = {kF + 2, kH + 2, kH + 2};
-    for (int b = 0; b < 3; ++b) {
-        MlpOff* ms[2] = {&L.edge[b], &L.node[b]};
-        const int ins[2] = {ein[b], nin[b]};
-        const int outs[2] = {1, kH};
-        for (int t = 0; t < 2; ++t) {
-            ms[t]->in = ins[t];
-            ms[t]->out = outs[t];
-            ms[t]->w1 = off;
-            off += kH * ins[t];
-            ms[t]->b1 = off;
-            off += kH;
-            ms[t]->w2 = off;
-            off += outs[t] * kH;
-            ms[t]->b2 = off;
-            off += outs[t];
-        }
-    }
-    return L;
+    for (int i = 0; i < b; ++i) off += mlp_size(edge_in(i), 1) + mlp_size(node_in(i), kH);
+    return off;
 }
+constexpr int node_off(int b) { return edge_off(b) + mlp_size(edge_in(b), 1); }
+static_assert(node_off(2) + mlp_size(node_in(2), kH) == 997, "parameter layout");
 
-// y = W2 tanh(W1 x + b1) + b2 (mlp_apply, src/gnn.cpp:43-57)
-template <int IN, int OUT>
-__device__ __forceinline__ void mlp(const MlpOff m, const double* x, double* y) {
+// y = W2 tanh(W1 x + b1) + b2 (mlp_apply, src/gnn.cpp:43-57), same
+// accumulation order as the reference (bias first, then inputs in order)
+template <int OFF, int IN, int OUT>
+__device__ __forceinline__ void mlp(const double* x, double* y) {
+    constexpr int W1 = OFF, B1 = OFF + kH * IN, W2 = B1 + kH, B2 = W2 + OUT * kH;
+    // inputs outer, hidden units inner: kH independent FMA chains (each in
+    // the reference's order: bias, then inputs 0..IN-1), every input
+    // consumed once -- no input vector kept live across the hidden units
     double hid[kH];
 #pragma unroll
-    for (int h = 0; h < kH; ++h) {
-        double acc = c_p[m.b1 + h];
+    for (int h = 0; h < kH; ++h) hid[h] = c_p[B1 + h];
 #pragma unroll
-        for (int i = 0; i < IN; ++i) acc = fma(c_p[m.w1 + h * IN + i], x[i], acc);
-        hid[h] = tanh(acc);
-    }
+    for (int i = 0; i < IN; ++i)
+#pragma unroll
+        for (int h = 0; h < kH; ++h) hid[h] = fma(c_p[W1 + h * IN + i], x[i], hid[h]);
+#pragma unroll
+    for (int h = 0; h < kH; ++h) hid[h] = tanh(hid[h]);
 #pragma unroll
     for (int o = 0; o < OUT; ++o) {
-        double acc = c_p[m.b2 + o];
+        double acc = c_p[B2 + o];
 #pragma unroll
-        for (int h = 0; h < kH; ++h) acc = fma(c_p[m.w2 + o * kH + h], hid[h], acc);
+        for (int h = 0; h < kH; ++h) acc = fma(c_p[W2 + o * kH + h], hid[h], acc);
         y[o] = acc;
     }
 }
@@ -198,47 +188,54 @@ __global__ void count_kernel(int64_t n, const int64_t* __restrict__ lrp, const i
 }
 
 // ------------------------------------------------------------ message passing
-// Edge updater: lane group of G lanes per row, lanes over the row's edges.
-template <int XW, bool FIRST, int G>
-__global__ void __launch_bounds__(256)
-edge_kernel(int64_t n, MlpOff m, const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
-            const double* __restrict__ x, const double* __restrict__ ef,
-            const double* __restrict__ eprev, double* __restrict__ eout, int* __restrict__ bad) {
-    constexpr int IN = (FIRST ? 1 : 2) + 2 * XW;
-    const int64_t gid = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G;
-    const int gl = threadIdx.x % G;
-    const int64_t ngroups = static_cast<int64_t>(gridDim.x) * blockDim.x / G;
+// Row index of every L entry (the edge's target node), for the flat edge
+// kernel: one warp per row writes its entries.
+__global__ void edge_rows_kernel(int64_t n, const int64_t* __restrict__ lrp, int32_t* __restrict__ erow) {
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= n) return;
+    for (int64_t k = lrp[i] + (threadIdx.x & 31); k < lrp[i + 1]; k += 32) erow[k] = static_cast<int32_t>(i);
+}
+
+// Edge updater: one thread per edge of the flat L entry list (every lane
+// busy whatever the row lengths), edge (i, j) = (erow[k], lcols[k]).
+// Consecutive edges share their row, so x_i is an L1 broadcast; x_j is an
+// L2-resident gather (mesh ordering keeps neighbours close).
+template <int BLK>
+__global__ void __launch_bounds__(256, 2)
+edge_kernel(int64_t ne, const int32_t* __restrict__ erow, const int32_t* __restrict__ lcols,
+            const double* __restrict__ x, const double* __restrict__ ef, const double* __restrict__ eprev,
+            double* __restrict__ eout, int* __restrict__ bad) {
+    constexpr bool FIRST = BLK == 0;
+    constexpr int XW = FIRST ? kF : kH;
+    constexpr int IN = edge_in(BLK);
     bool nonfinite = false;
-    for (int64_t i = gid; i < n; i += ngroups) {
-        double xi[XW];
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < ne;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = erow[k], j = lcols[k];
+        double in[IN];
+        int w = 0;
+        if (!FIRST) in[w++] = eprev[k];
+        in[w++] = ef[k];
 #pragma unroll
-        for (int c = 0; c < XW; ++c) xi[c] = x[i * XW + c];
-        for (int64_t k = lrp[i] + gl; k < lrp[i + 1]; k += G) {
-            const int32_t j = lcols[k];
-            double in[IN];
-            int w = 0;
-            if (!FIRST) in[w++] = eprev[k];
-            in[w++] = ef[k];
+        for (int c = 0; c < XW; ++c) in[w + c] = x[i * XW + c];
 #pragma unroll
-            for (int c = 0; c < XW; ++c) in[w + c] = xi[c];
-#pragma unroll
-            for (int c = 0; c < XW; ++c) in[w + XW + c] = x[static_cast<int64_t>(j) * XW + c];
-            double y;
-            mlp<IN, 1>(m, in, &y);
-            eout[k] = y;
-            nonfinite |= !isfinite(y);
-        }
+        for (int c = 0; c < XW; ++c) in[w + XW + c] = x[j * XW + c];
+        double y;
+        mlp<edge_off(BLK), IN, 1>(in, &y);
+        eout[k] = y;
+        nonfinite |= !isfinite(y);
     }
     if (nonfinite) *bad = 1;
 }
 
 // Node updater with the fused sum/mean aggregation.
-template <int XW>
+template <int BLK>
 __global__ void __launch_bounds__(256)
-node_kernel(int64_t n, MlpOff m, const int64_t* __restrict__ lrp, const int64_t* __restrict__ urp,
+node_kernel(int64_t n, const int64_t* __restrict__ lrp, const int64_t* __restrict__ urp,
             const int64_t* __restrict__ u2l, const double* __restrict__ cnt,
             const double* __restrict__ x, const double* __restrict__ e, double* __restrict__ xo,
             int* __restrict__ bad) {
+    constexpr int XW = BLK == 0 ? kF : kH;
     const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (v >= n) return;
     double s = 0.0;
@@ -250,7 +247,7 @@ node_kernel(int64_t n, MlpOff m, const int64_t* __restrict__ lrp, const int64_t*
     in[XW] = s;
     in[XW + 1] = cnt[v] > 0.0 ? s / cnt[v] : 0.0;
     double y[kH];
-    mlp<XW + 2, kH>(m, in, y);
+    mlp<node_off(BLK), node_in(BLK), kH>(in, y);
     bool nonfinite = false;
 #pragma unroll
     for (int h = 0; h < kH; ++h) {
@@ -271,16 +268,16 @@ __global__ void output_kernel(int64_t n, const int64_t* __restrict__ lrp, double
 
 inline unsigned gfor(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
-template <int XW, bool FIRST>
-void launch_edge(int G, unsigned grid, cudaStream_t st, int64_t n, MlpOff m, const int64_t* lrp,
-                 const int32_t* lcols, const double* x, const double* ef, const double* eprev,
-                 double* eout, int* bad) {
-    switch (G) {
-        case 4: edge_kernel<XW, FIRST, 4><<<grid, 256, 0, st>>>(n, m, lrp, lcols, x, ef, eprev, eout, bad); break;
-        case 8: edge_kernel<XW, FIRST, 8><<<grid, 256, 0, st>>>(n, m, lrp, lcols, x, ef, eprev, eout, bad); break;
-        case 16: edge_kernel<XW, FIRST, 16><<<grid, 256, 0, st>>>(n, m, lrp, lcols, x, ef, eprev, eout, bad); break;
-        default: edge_kernel<XW, FIRST, 32><<<grid, 256, 0, st>>>(n, m, lrp, lcols, x, ef, eprev, eout, bad); break;
+template <int BLK>
+void launch_edge(int64_t ne, const int32_t* erow, const int32_t* lcols, const double* x, const double* ef,
+                 const double* eprev, double* eout, int* bad, cudaStream_t st) {
+    static unsigned grid = 0;
+    if (!grid) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_kernel<BLK>, 256, 0));
+        grid = static_cast<unsigned>(std::max(per_sm, 1) * sm_count() * 4);
     }
+    edge_kernel<BLK><<<grid, 256, 0, st>>>(ne, erow, lcols, x, ef, eprev, eout, bad);
     CK_LAUNCH();
 }
 
@@ -288,7 +285,6 @@ void launch_edge(int G, unsigned grid, cudaStream_t st, int64_t n, MlpOff m, con
 
 void gnn_forward(const Matrix& A, const Analysis& an, const Model& model, double* out,
                  double* sigma_out, cudaStream_t st) {
-    const Layout ly = make_layout();
     if (model.params.size() != 997) throw DimensionError("gnn: parameter vector has wrong length");
     CK(cudaMemcpyToSymbolAsync(c_p, model.params.data(), sizeof(double) * 997, 0,
                                cudaMemcpyHostToDevice, st));
@@ -351,26 +347,22 @@ void gnn_forward(const Matrix& A, const Analysis& an, const Model& model, double
     *sigma_out = sigma;
     count_kernel<<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, cnt.p);
     // ---- three message-passing blocks (gnn.cpp:162-205)
-    const double avg = static_cast<double>(ne) / static_cast<double>(n);
-    int G = 4;
-    while (G < 32 && G < avg) G *= 2;
-    const unsigned egrid = static_cast<unsigned>(sm_count() * 16);
+    DevBuf<int32_t> erow(ne);
+    edge_rows_kernel<<<gfor(n * 32, T), T, 0, st>>>(n, L.rp.p, erow.p);
+    CK_LAUNCH();
     DevBuf<double> e1(ne), e2(ne), xa(n * kH), xb(n * kH);
     DevBuf<int> bad(6);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int) * 6, st));
-    launch_edge<kF, true>(G, egrid, st, n, ly.edge[0], L.rp.p, L.cols.p, x0.p, ef.p, nullptr, e1.p, bad.p);
-    node_kernel<kF><<<gfor(n, T), T, 0, st>>>(n, ly.node[0], L.rp.p, U.rp.p, an.u2l.p, cnt.p, x0.p, e1.p,
-                                               xa.p, bad.p + 1);
+    launch_edge<0>(ne, erow.p, L.cols.p, x0.p, ef.p, nullptr, e1.p, bad.p, st);
+    node_kernel<0><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, x0.p, e1.p, xa.p, bad.p + 1);
     CK_LAUNCH();
-    launch_edge<kH, false>(G, egrid, st, n, ly.edge[1], L.rp.p, L.cols.p, xa.p, ef.p, e1.p, e2.p, bad.p + 2);
-    node_kernel<kH><<<gfor(n, T), T, 0, st>>>(n, ly.node[1], L.rp.p, U.rp.p, an.u2l.p, cnt.p, xa.p, e2.p,
-                                               xb.p, bad.p + 3);
+    launch_edge<1>(ne, erow.p, L.cols.p, xa.p, ef.p, e1.p, e2.p, bad.p + 2, st);
+    node_kernel<1><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, xa.p, e2.p, xb.p, bad.p + 3);
     CK_LAUNCH();
-    launch_edge<kH, false>(G, egrid, st, n, ly.edge[2], L.rp.p, L.cols.p, xb.p, ef.p, e2.p, out, bad.p + 4);
+    launch_edge<2>(ne, erow.p, L.cols.p, xb.p, ef.p, e2.p, out, bad.p + 4, st);
     // the final node state feeds nothing (gnn.cpp:199-205 computes it and
     // checks it for finiteness)
-    node_kernel<kH><<<gfor(n, T), T, 0, st>>>(n, ly.node[2], L.rp.p, U.rp.p, an.u2l.p, cnt.p, xb.p, out,
-                                               xa.p, bad.p + 5);
+    node_kernel<2><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, xb.p, out, xa.p, bad.p + 5);
     CK_LAUNCH();
     int hb[6];
     CK(cudaMemcpyAsync(hb, bad.p, sizeof hb, cudaMemcpyDeviceToHost, st));

@@ -1,8 +1,2 @@
-# developer probe: staggered polls + ncu full of the dominant kernels
-for env in "PCLAB_POLL=0" "PCLAB_POLL=1" "PCLAB_POLL=1 PCLAB_TRSV_TUNE=20480" "PCLAB_POLL=1 PCLAB_TRSV_TUNE=51200"; do
-  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/exp10.log 2>&1
-done
-python tools/run_kernels.py elasticity_q1_118 0 1 gnnic > gpurun_out/rk.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on \
-      -k regex:"bsr_trsv_kernel|k_spmv_bsr_pap|edge_kernel|node_kernel|ic0_kernel|features_kernel" -c 14 \
-      -o gpurun_out/full python tools/run_kernels.py elasticity_q1_118 0 1 gnnic > gpurun_out/ncu_full.log 2>&1
+timeout 300 python tools/gnn_time.py elasticity_q1_118 > gpurun_out/gnn_time.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "gnn or config1" > gpurun_out/tgnn.log 2>&1
