@@ -421,9 +421,9 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
                                           int64_t nwarps, int tune, long long* trace) {
     // tune: sleep_ns << 8 | experiment bits (developer timing probes that
     // give WRONG results: 1 = matrix values from one cached line, 2 = no
-    // dependency waits)
+    // dependency waits, 4 = no dependency loads at all)
     const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
-    const bool exp_vals = tune & 1, exp_nowait = tune & 2;
+    const bool exp_vals = tune & 1, exp_nowait = tune & 2, exp_nox = tune & 4;
     constexpr int G = 32 / LG;
     constexpr int NIB = BS * (BS - 1) / 2;
     const int lane = threadIdx.x & 31;
@@ -498,7 +498,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
                     for (int c = 0; c < BS; ++c)
                         a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
 #pragma unroll
-                for (int c = 0; c < BS; ++c) xv[c] = ld_relaxed(out + xc + c);
+                for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
                 if (exp_nowait)
 #pragma unroll
                     for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
