@@ -22,6 +22,7 @@
 #define BSR_CTAS 5
 #endif
 
+
 namespace pclab_b200 {
 
 // Rows per warp = 32 / LPR; each lane group of LPR lanes reduces one row
@@ -414,6 +415,133 @@ __device__ __forceinline__ int slot_nb(const BsrSlot& m) {
 // and every load is issued a whole item before its value is needed:
 //   item k+3: slot record        item k+2: entries prefetched into L1
 //   item k+1: right-hand side    item k:   entries, dependency polls
+// One item of the node-blocked sweep: this lane group's block `m` (rows
+// r0..r0+BS-1, right-hand side rc), lane gl owning neighbour blocks gl,
+// gl+LG, ...: stream the 3x3 values, poll the neighbours' values, reduce,
+// solve the diagonal block, publish, re-arm `reset`. `flags` = experiment
+// bits of the tune word (see bsr_sweep).
+template <int LG, int BS, bool UPPER>
+__device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS], const int32_t* __restrict__ bcol,
+                                         const double* __restrict__ vals, const double* __restrict__ invd,
+                                         double* out, double* reset, unsigned sleep_ns, int flags, int64_t it,
+                                         long long* trace, long long tr0) {
+    constexpr int NIB = BS * (BS - 1) / 2;
+    const bool exp_vals = flags & 1, exp_nowait = flags & 2, exp_nox = flags & 4;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % LG;
+    const bool active = m.blk >= 0;
+    const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
+    int64_t mrp[BS + 1];
+    slot_rows<BS>(m, mrp);
+    // off-block entries of row t start at ob[t]; nb neighbour blocks
+    int64_t ob[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
+    const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
+    double binv[BS], bin[NIB > 0 ? NIB : 1];
+    if (active && gl == 0) {
+#pragma unroll
+        for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
+        int q = 0;
+#pragma unroll
+        for (int t = 0; t < BS; ++t)
+#pragma unroll
+            for (int s = 0; s < BS; ++s) {
+                if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
+                if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
+            }
+    }
+    double acc[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+    const int nbmax = __reduce_max_sync(0xffffffffu, nb);
+    int rounds = 0;
+    for (int n0 = 0; n0 < nbmax; n0 += LG) {
+        const int n = n0 + gl;
+        const bool own = n < nb;
+        double a[BS][BS], xv[BS];
+        int32_t xc = 0;
+        if (own) {
+            xc = ld_stream(bcol + m.bp + n);
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+                    a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
+#pragma unroll
+            for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
+            if (exp_nowait)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
+        } else {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) {
+                xv[t] = 0.0;
+#pragma unroll
+                for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
+            }
+        }
+        bool pend = false;
+#pragma unroll
+        for (int c = 0; c < BS; ++c) pend |= own && is_pending(xv[c]);
+        while (__any_sync(0xffffffffu, pend)) {
+            ++rounds;
+            if (sleep_ns) __nanosleep(sleep_ns);
+            pend = false;
+#pragma unroll
+            for (int c = 0; c < BS; ++c)
+                if (own && is_pending(xv[c])) {
+                    xv[c] = ld_relaxed(out + xc + c);
+                    pend |= is_pending(xv[c]);
+                }
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t)
+#pragma unroll
+            for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+    }
+    long long trg = 0;
+    if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
+#pragma unroll
+    for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+    if (active && gl == 0) {
+        double xb[BS];
+        if (!UPPER) {
+            int q = 0;
+#pragma unroll
+            for (int t = 0; t < BS; ++t) {
+                double s = rc[t] - acc[t];
+#pragma unroll
+                for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
+                xb[t] = s * binv[t];
+            }
+        } else {
+#pragma unroll
+            for (int t = BS - 1; t >= 0; --t) {
+                double s = rc[t] - acc[t];
+                int q = 0;
+#pragma unroll
+                for (int r = 0; r < t; ++r) q += BS - 1 - r;
+#pragma unroll
+                for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
+                xb[t] = s * binv[t];
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+    }
+    if (trace && lane == 0) {
+        long long tr2;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
+        trace[4LL * it + 0] = tr0;
+        trace[4LL * it + 1] = trg;  // no separate critical poll: values in hand
+        trace[4LL * it + 2] = tr2;
+        trace[4LL * it + 3] = min(rounds, 1023);
+    }
+    __syncwarp();
+    if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+}
+
 template <int LG, int BS, bool UPPER>
 __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ srec, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
@@ -423,9 +551,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     // give WRONG results: 1 = matrix values from one cached line, 2 = no
     // dependency waits, 4 = no dependency loads at all)
     const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
-    const bool exp_vals = tune & 1, exp_nowait = tune & 2, exp_nox = tune & 4;
     constexpr int G = 32 / LG;
-    constexpr int NIB = BS * (BS - 1) / 2;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     int64_t it = warp;
@@ -458,117 +584,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         prefetch(m2);
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
-        const bool active = m.blk >= 0;
-        const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
-        int64_t mrp[BS + 1];
-        slot_rows<BS>(m, mrp);
-        // off-block entries of row t start at ob[t]; nb neighbour blocks
-        int64_t ob[BS];
-#pragma unroll
-        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
-        const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
-        double binv[BS], bin[NIB > 0 ? NIB : 1];
-        if (active && gl == 0) {
-#pragma unroll
-            for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
-            int q = 0;
-#pragma unroll
-            for (int t = 0; t < BS; ++t)
-#pragma unroll
-                for (int s = 0; s < BS; ++s) {
-                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
-                    if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
-                }
-        }
-        double acc[BS];
-#pragma unroll
-        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
-        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
-        int rounds = 0;
-        for (int n0 = 0; n0 < nbmax; n0 += LG) {
-            const int n = n0 + gl;
-            const bool own = n < nb;
-            double a[BS][BS], xv[BS];
-            int32_t xc = 0;
-            if (own) {
-                xc = ld_stream(bcol + m.bp + n);
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c)
-                        a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
-#pragma unroll
-                for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
-                if (exp_nowait)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
-            } else {
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    xv[t] = 0.0;
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
-                }
-            }
-            bool pend = false;
-#pragma unroll
-            for (int c = 0; c < BS; ++c) pend |= own && is_pending(xv[c]);
-            while (__any_sync(0xffffffffu, pend)) {
-                ++rounds;
-                if (sleep_ns) __nanosleep(sleep_ns);
-                pend = false;
-#pragma unroll
-                for (int c = 0; c < BS; ++c)
-                    if (own && is_pending(xv[c])) {
-                        xv[c] = ld_relaxed(out + xc + c);
-                        pend |= is_pending(xv[c]);
-                    }
-            }
-#pragma unroll
-            for (int t = 0; t < BS; ++t)
-#pragma unroll
-                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
-        }
-        long long trg = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
-#pragma unroll
-        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
-        if (active && gl == 0) {
-            double xb[BS];
-            if (!UPPER) {
-                int q = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    double s = rhs0[t] - acc[t];
-#pragma unroll
-                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            } else {
-#pragma unroll
-                for (int t = BS - 1; t >= 0; --t) {
-                    double s = rhs0[t] - acc[t];
-                    int q = 0;
-#pragma unroll
-                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
-        }
-        if (trace && lane == 0) {
-            long long tr2;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
-            trace[4LL * it + 0] = tr0;
-            trace[4LL * it + 1] = trg;  // no separate critical poll: values in hand
-            trace[4LL * it + 2] = tr2;
-            trace[4LL * it + 3] = min(rounds, 1023);
-        }
-        __syncwarp();
-        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+        bsr_item<LG, BS, UPPER>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0);
         it += nwarps;
         m = m1;
         m1 = m2;
