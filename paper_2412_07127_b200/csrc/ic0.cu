@@ -19,6 +19,7 @@
 // entries they read, so rows pipeline across levels without barriers.
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "core.h"
@@ -130,6 +131,144 @@ ic0_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict__ slo
     }
 }
 
+// ---------------------------------------------------------------- masks
+// Symbolic half of the mask factorisation (rows of <= 64 entries). For
+// off-diagonal entry t of row i (column j): bit u of mu[k] is set when
+// column c_u (u < t) of row i also occurs in row j, and bit p of mj[k]
+// marks that occurrence's position p in row j -- the k-th set bit of mu
+// pairs with the k-th set bit of mj. This is the reference's merge
+// (precond.cpp:40-60) done once, without dependencies: warp per row, row
+// i's columns in shared memory, lane t walks row j.
+__global__ void __launch_bounds__(256)
+ic0_masks(int64_t n, const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
+          unsigned long long* __restrict__ mu, unsigned long long* __restrict__ mj) {
+    __shared__ int32_t rowc[8][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const int64_t beg = lrp[i];
+    const int nd = static_cast<int>(lrp[i + 1] - beg) - 1;
+    for (int t = lane; t < nd; t += 32) rowc[w][t] = lcols[beg + t];
+    __syncwarp();
+    for (int t = lane; t < nd; t += 32) {
+        const int32_t j = rowc[w][t];
+        const int64_t rj = lrp[j];
+        const int nj = static_cast<int>(lrp[j + 1] - rj) - 1;
+        unsigned long long bu = 0, bj = 0;
+        int u = 0, q = 0;
+        int32_t cq = q < nj ? lcols[rj] : INT_MAX;
+        while (u < t && q < nj) {
+            const int32_t cu = rowc[w][u];
+            if (cu < cq) {
+                ++u;
+            } else if (cq < cu) {
+                ++q;
+                cq = q < nj ? lcols[rj + q] : INT_MAX;
+            } else {
+                bu |= 1ULL << u;
+                bj |= 1ULL << q;
+                ++u;
+                ++q;
+                cq = q < nj ? lcols[rj + q] : INT_MAX;
+            }
+        }
+        mu[beg + t] = bu;
+        mj[beg + t] = bj;
+    }
+}
+
+// Numeric half: the ic0_kernel schedule (warp per row, rows in (level,
+// index) order, lane t owns entry t, step u finalises entry u and
+// broadcasts l_{i c_u}), but a lane learns from its masks whether step u
+// touches it and where l_{j c_u} sits in row j -- no merge walk. The value
+// of the next match is loaded one match ahead. Same per-entry operation
+// order as the reference, explicitly rounded: bit-identical.
+template <int C>
+__global__ void __launch_bounds__(256)
+ic0_mask_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict__ slots,
+                const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
+                const double* __restrict__ avals, const unsigned long long* __restrict__ mu,
+                const unsigned long long* __restrict__ mj, double shift, double* v,
+                unsigned long long* fail_row, unsigned* counter) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned it = 0;
+        if (lane == 0) it = atomicAdd(counter, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nitems * bs) return;
+        const int64_t item = it / bs;
+        const int t_row = static_cast<int>(it % bs);
+        for (int g = 0; g < per_item; ++g) {
+            const int32_t blk = slots[item * per_item + g];
+            if (blk < 0) continue;
+            const int64_t i = static_cast<int64_t>(blk) * bs + t_row;
+            const int64_t beg = lrp[i];
+            const int nd = static_cast<int>(lrp[i + 1] - beg) - 1;
+            double s[C], dj[C], wn[C];
+            unsigned long long bu[C], bj[C];
+            int64_t rj[C], dpos[C];
+            int32_t jc[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int t = lane + 32 * c;
+                bu[c] = bj[c] = 0;
+                s[c] = dj[c] = wn[c] = 0.0;
+                rj[c] = dpos[c] = 0;
+                jc[c] = 0;
+                if (t < nd) {
+                    jc[c] = lcols[beg + t];
+                    s[c] = avals[beg + t];
+                    bu[c] = mu[beg + t];
+                    bj[c] = mj[beg + t];
+                    rj[c] = lrp[jc[c]];
+                    dpos[c] = lrp[jc[c] + 1] - 1;  // l_jj
+                    dj[c] = ld_relaxed(v + dpos[c]);
+                    if (bj[c]) wn[c] = ld_relaxed(v + rj[c] + (__ffsll(static_cast<long long>(bj[c])) - 1));
+                }
+            }
+            double diag_acc = 0.0;
+            for (int u = 0; u < nd; ++u) {
+                const int owner = u & 31, oc = u >> 5;
+                double l = 0.0;
+                int32_t cu = 0;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if (c == oc && lane == owner) {
+                        double d = dj[c];
+                        while (is_pending(d)) d = ld_relaxed(v + dpos[c]);
+                        l = __ddiv_rn(s[c], d);
+                        st_relaxed(v + beg + u, l);
+                        cu = jc[c];
+                    }
+                l = __shfl_sync(0xffffffffu, l, owner);
+                (void)cu;
+                diag_acc = __dadd_rn(diag_acc, __dmul_rn(l, l));
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    if ((bu[c] >> u) & 1ULL) {
+                        const int pos = __ffsll(static_cast<long long>(bj[c])) - 1;
+                        double w = wn[c];
+                        while (is_pending(w)) w = ld_relaxed(v + rj[c] + pos);
+                        s[c] = __dsub_rn(s[c], __dmul_rn(l, w));
+                        bj[c] &= bj[c] - 1;
+                        if (bj[c]) wn[c] = ld_relaxed(v + rj[c] + (__ffsll(static_cast<long long>(bj[c])) - 1));
+                    }
+                }
+            }
+            if (lane == 0) {
+                const double sd = __dsub_rn(__dadd_rn(avals[beg + nd], shift), diag_acc);
+                if (!(sd > 0.0)) {
+                    st_relaxed(v + beg + nd, __longlong_as_double(static_cast<long long>(kBroken)));
+                    atomicMin(fail_row, static_cast<unsigned long long>(i));
+                } else {
+                    st_relaxed(v + beg + nd, __dsqrt_rn(sd));
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 __global__ void row_stats(int64_t n, const int64_t* __restrict__ rp, const double* __restrict__ lv,
                           unsigned* maxlen, unsigned long long* maxdiag) {
     unsigned ml = 0;
@@ -179,15 +318,30 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
     // the forward-sweep block schedule: a warp per item, rows in order
     const Schedule& s = an.blk_lo;
     const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
-    const int64_t blocks = (static_cast<int64_t>(6.0 * per_level) + 8) / 8;
+    static const double depth = getenv("PCLAB_IC0_DEPTH") ? atof(getenv("PCLAB_IC0_DEPTH")) : 6.0;
+    const int64_t blocks = (static_cast<int64_t>(depth * per_level) + 8) / 8;
     const unsigned grid = static_cast<unsigned>(
         std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * 8));
+    // rows of <= 64 entries: symbolic masks once, then the mask kernel
+    // (PCLAB_IC0_MASKS=0 keeps the merge-walk kernel)
+    static const bool masks_env = !(getenv("PCLAB_IC0_MASKS") && atoi(getenv("PCLAB_IC0_MASKS")) == 0);
+    const bool use_masks = masks_env && maxlen <= 64;
+    DevBuf<unsigned long long> mu, mj;
+    if (use_masks) {
+        mu.alloc(L.nnz);
+        mj.alloc(L.nnz);
+        ic0_masks<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(n, L.rp.p, L.cols.p, mu.p, mj.p);
+        CK_LAUNCH();
+    }
     for (int attempt = 0;; ++attempt) {
         const double shift = attempt == 0 ? 0.0 : alpha0 * static_cast<double>(1 << (attempt - 1));
         fill_pending(out, L.nnz, st);
         CK(cudaMemsetAsync(fail.p, 0xff, sizeof(unsigned long long), st));
         CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
-        if (maxlen <= 64)
+        if (use_masks)
+            ic0_mask_kernel<2><<<grid, 256, 0, st>>>(s.nitems, s.per_item, s.bs, s.slots.p, L.rp.p, L.cols.p,
+                                                      L.vals.p, mu.p, mj.p, shift, out, fail.p, ctr.p);
+        else if (maxlen <= 64)
             ic0_kernel<2><<<grid, 256, 0, st>>>(s.nitems, s.per_item, s.bs, s.slots.p, L.rp.p, L.cols.p,
                                                  L.vals.p, shift, out, fail.p, ctr.p);
         else if (maxlen <= 128)

@@ -1,4 +1,2 @@
-for env in "PCLAB_SMP=0" "PCLAB_SMP=1" "PCLAB_SMP=1 PCLAB_TRSV_DEPTH=4" "PCLAB_SMP=1 PCLAB_TRSV_TUNE=2"; do
-  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/smp.log 2>&1
-done
-PCLAB_SMP=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/tsmp.log 2>&1
+python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/rk2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"ic0|gather_kernel|invd_kernel|row_stats" -c 6 -o gpurun_out/ic0prof python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/ncu_ic0.log 2>&1
