@@ -139,13 +139,20 @@ ic0_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict__ slo
 // pairs with the k-th set bit of mj. This is the reference's merge
 // (precond.cpp:40-60) done once, without dependencies: warp per row, row
 // i's columns in shared memory, lane t walks row j.
+//
+// Node-blocked L (Analysis::bsr, bs > 1): the bs rows of a block share their
+// off-block columns, so row bs*b + t's masks for its first nd0 entries
+// equal row bs*b's, and its in-block entry s (column bs*b + s) meets every
+// earlier entry of both rows: mu = mj = (1 << p) - 1 at position p. One warp
+// per block then merges only row bs*b.
 __global__ void __launch_bounds__(256)
-ic0_masks(int64_t n, const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
+ic0_masks(int64_t nunits, int bs, const int64_t* __restrict__ lrp, const int32_t* __restrict__ lcols,
           unsigned long long* __restrict__ mu, unsigned long long* __restrict__ mj) {
     __shared__ int32_t rowc[8][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (i >= n) return;
+    const int64_t unit = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (unit >= nunits) return;
+    const int64_t i = unit * bs;  // bs = 1: every row is a unit
     const int64_t beg = lrp[i];
     const int nd = static_cast<int>(lrp[i + 1] - beg) - 1;
     for (int t = lane; t < nd; t += 32) rowc[w][t] = lcols[beg + t];
@@ -172,8 +179,21 @@ ic0_masks(int64_t n, const int64_t* __restrict__ lrp, const int32_t* __restrict_
                 cq = q < nj ? lcols[rj + q] : INT_MAX;
             }
         }
-        mu[beg + t] = bu;
-        mj[beg + t] = bj;
+        for (int r = 0; r < bs; ++r) {  // rows of the block share these entries
+            const int64_t br = lrp[i + r];
+            mu[br + t] = bu;
+            mj[br + t] = bj;
+        }
+    }
+    // in-block entries of rows t >= 1 (position p = nd + s, column i + s)
+    for (int r = 1; r < bs; ++r) {
+        const int64_t br = lrp[i + r];
+        for (int sidx = lane; sidx < r; sidx += 32) {
+            const int p = nd + sidx;
+            const unsigned long long m = p >= 64 ? ~0ULL : (1ULL << p) - 1;
+            mu[br + p] = m;
+            mj[br + p] = m;
+        }
     }
 }
 
@@ -330,7 +350,10 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
     if (use_masks) {
         mu.alloc(L.nnz);
         mj.alloc(L.nnz);
-        ic0_masks<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(n, L.rp.p, L.cols.p, mu.p, mj.p);
+        const int mbs = an.bsr ? an.bs : 1;
+        const int64_t units = n / mbs;
+        ic0_masks<<<static_cast<unsigned>((units * 32 + 255) / 256), 256, 0, st>>>(units, mbs, L.rp.p, L.cols.p,
+                                                                                   mu.p, mj.p);
         CK_LAUNCH();
     }
     for (int attempt = 0;; ++attempt) {

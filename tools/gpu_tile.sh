@@ -1,2 +1,2 @@
-python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/rk2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"ic0|gather_kernel|invd_kernel|row_stats" -c 6 -o gpurun_out/ic0prof python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/ncu_ic0.log 2>&1
+timeout 300 python tools/gnn_time.py elasticity_q1_118 > gpurun_out/ic0m2.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "ic0 or config or fixture or acceptance or pcg" > gpurun_out/tic02.log 2>&1
