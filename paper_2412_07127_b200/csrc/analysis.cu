@@ -165,6 +165,21 @@ __global__ void kahn_init(int64_t nb, int bs, const int64_t* __restrict__ prp,
     }
 }
 
+// Node-blocked variant: predecessors / successors are the block columns
+// (one entry per neighbour block instead of bs x bs scalar entries).
+__global__ void kahn_init_bc(int64_t nb, const int64_t* __restrict__ pbp, int32_t* __restrict__ indeg,
+                             int32_t* __restrict__ level, int32_t* __restrict__ fr, KState* ks) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int cnt = static_cast<int>(pbp[b + 1] - pbp[b]);
+    indeg[b] = cnt;
+    level[b] = -1;
+    if (cnt == 0) {
+        level[b] = 0;
+        fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(b);
+    }
+}
+
 // warp per frontier block, lanes over the successor entries
 __global__ void kahn_step(int bs, const int64_t* __restrict__ srp, const int32_t* __restrict__ scols,
                           bool upper, int32_t* __restrict__ indeg, int32_t* __restrict__ level,
@@ -189,7 +204,11 @@ __global__ void kahn_step(int bs, const int64_t* __restrict__ srp, const int32_t
 }
 
 // All levels in one cooperative launch: process the frontier, grid barrier,
-// thread 0 advances the frontier window, grid barrier.
+// thread 0 advances the frontier window, grid barrier. BC: successors from
+// a block-column view (sbp/sbcol), one atomic per neighbour block -- a
+// frontier block's successors fit one warp round, so a level costs one
+// atomic round trip instead of one per 32 scalar entries.
+template <bool BC>
 __global__ void kahn_persistent(int bs, const int64_t* __restrict__ srp,
                                 const int32_t* __restrict__ scols, bool upper,
                                 int32_t* __restrict__ indeg, int32_t* __restrict__ level,
@@ -205,15 +224,25 @@ __global__ void kahn_persistent(int bs, const int64_t* __restrict__ srp,
         const int nl = vk->lvl + 1;
         for (unsigned long long p = beg + w0; p < end; p += nw) {
             const int64_t b = __ldcg(fr + p);  // appended by other CTAs: bypass L1
-            for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
-                for (int64_t k = srp[i] + lane; k < srp[i + 1]; k += 32) {
+            if (BC) {
+                for (int64_t k = srp[b] + lane; k < srp[b + 1]; k += 32) {
                     const int64_t jb = scols[k] / bs;
-                    if (!is_pred(b, jb, upper)) continue;
                     if (atomicSub(&indeg[jb], 1) == 1) {
                         level[jb] = nl;
                         fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(jb);
                     }
                 }
+            } else {
+                for (int64_t i = b * bs; i < (b + 1) * bs; ++i)
+                    for (int64_t k = srp[i] + lane; k < srp[i + 1]; k += 32) {
+                        const int64_t jb = scols[k] / bs;
+                        if (!is_pred(b, jb, upper)) continue;
+                        if (atomicSub(&indeg[jb], 1) == 1) {
+                            level[jb] = nl;
+                            fr[atomicAdd(&ks->tail, 1ULL)] = static_cast<int32_t>(jb);
+                        }
+                    }
+            }
         }
         g.sync();
         if (g.thread_rank() == 0) {
@@ -447,7 +476,7 @@ inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t
 }  // namespace
 
 void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
-                    cudaStream_t st) {
+                    cudaStream_t st, const BlockCols* pbc, const BlockCols* sbc) {
     const int64_t n = pred.n;
     s.bs = bs;
     s.nblocks = n / bs;
@@ -455,30 +484,35 @@ void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, 
     s.crit.alloc(std::max<int64_t>(s.nblocks, 1));
     if (s.nblocks == 0) return;
     const int64_t nb = s.nblocks;
+    const bool bc = pbc && sbc && pbc->bp.p && sbc->bp.p;
     DevBuf<int32_t> indeg(nb), fr(nb);
     DevBuf<KState> ks(1);
     CK(cudaMemsetAsync(ks.p, 0, sizeof(KState), st));
-    kahn_init<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, indeg.p, s.level.p,
-                                                 fr.p, ks.p);
+    if (bc)
+        kahn_init_bc<<<grid_for(nb, 256), 256, 0, st>>>(nb, pbc->bp.p, indeg.p, s.level.p, fr.p, ks.p);
+    else
+        kahn_init<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, indeg.p, s.level.p,
+                                                     fr.p, ks.p);
     CK_LAUNCH();
     kahn_start<<<1, 1, 0, st>>>(ks.p);  // frontier of level 0 = the seeds
     CK_LAUNCH();
     // one cooperative persistent launch: a grid barrier per level instead
     // of a kernel launch per level
+    auto kern = bc ? kahn_persistent<true> : kahn_persistent<false>;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kahn_persistent, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
     const unsigned grid = static_cast<unsigned>(sm_count() * std::max(1, std::min(per_sm, 4)));
     {
         int bs_ = bs;
-        const int64_t* srp = succ.rp.p;
-        const int32_t* scols = succ.cols.p;
+        const int64_t* srp = bc ? sbc->bp.p : succ.rp.p;
+        const int32_t* scols = bc ? sbc->bcol.p : succ.cols.p;
         bool up = upper;
         int32_t* ind = indeg.p;
         int32_t* lev = s.level.p;
         int32_t* frp = fr.p;
         KState* ksp = ks.p;
         void* args[] = {&bs_, &srp, &scols, &up, &ind, &lev, &frp, &ksp};
-        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kahn_persistent), grid, 256, args, 0, st));
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, 256, args, 0, st));
         CK_LAUNCH();
     }
     KState h{};
@@ -494,8 +528,9 @@ void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, 
 }
 
 static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, int lanes,
-                           Schedule& s, cudaStream_t st) {
-    compute_levels(pred, succ, bs, upper, s, st);
+                           Schedule& s, cudaStream_t st, const BlockCols* pbc = nullptr,
+                           const BlockCols* sbc = nullptr) {
+    compute_levels(pred, succ, bs, upper, s, st, pbc, sbc);
     s.lanes = lanes;
     s.per_item = 32 / lanes;
     const int64_t nb = s.nblocks;
@@ -785,6 +820,8 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, st));
     auto an = std::make_unique<Analysis>();
+    static std::atomic<uint64_t> next_id{1};
+    an->id = next_id++;
     DevCsr& L = an->lower;
     DevCsr& U = an->upper;
     L.n = U.n = n;
@@ -852,12 +889,14 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     static const bool rr_on = !(getenv("PCLAB_RR") && atoi(getenv("PCLAB_RR")) == 0);
     an->blk_lo.need_crit = an->blk_up.need_crit =
         (!an->bsr && !rr_on) || getenv("PCLAB_TRSV_TRACE") != nullptr;
-    build_schedule(L, U, bs, false, lanes, an->blk_lo, st);
-    build_schedule(U, L, bs, true, lanes, an->blk_up, st);
-    if (an->bsr) {
+    if (an->bsr) {  // block columns first: the levelling walks them
         build_block_cols(L, bs, 0, an->lbc, st);
         build_block_cols(U, bs, 1, an->ubc, st);
     }
+    build_schedule(L, U, bs, false, lanes, an->blk_lo, st, an->bsr ? &an->lbc : nullptr,
+                   an->bsr ? &an->ubc : nullptr);
+    build_schedule(U, L, bs, true, lanes, an->blk_up, st, an->bsr ? &an->ubc : nullptr,
+                   an->bsr ? &an->lbc : nullptr);
     an->rr = false;
     DevBuf<int> bad(1);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));

@@ -148,6 +148,7 @@ struct Analysis {
     bool fused_up = false;
     DevBuf<int32_t> mv_order;
     double ms = 0.0;         // wall time of the analysis (CUDA events)
+    uint64_t id = 0;         // unique per analysis (IC(0) mask cache key)
 };
 
 struct Matrix {
@@ -208,7 +209,7 @@ bool matrix_symmetric(Matrix& a, cudaStream_t st);
 // analysis.cu
 Analysis& ensure_analysis(Matrix& a, cudaStream_t st);
 void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
-                    cudaStream_t st);
+                    cudaStream_t st, const BlockCols* pbc = nullptr, const BlockCols* sbc = nullptr);
 
 // ic0.cu: factor values on an.lower's pattern; returns shift attempts
 int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st);

@@ -1,2 +1,2 @@
-timeout 300 python tools/gnn_time.py elasticity_q1_118 > gpurun_out/ic0m2.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "ic0 or config or fixture or acceptance or pcg" > gpurun_out/tic02.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bk4.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > gpurun_out/tk4.log 2>&1
