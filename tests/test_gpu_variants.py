@@ -88,3 +88,31 @@ def test_tiled_sweep_bit_identical_to_round_robin():
         assert out.returncode == 0, out.stdout + out.stderr
         outs.append(out.stdout.strip())
     assert len(set(outs)) == 1, outs
+
+
+IC0 = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_2412_07127_b200 as P
+h = hashlib.sha256()
+for w in (P.workloads.by_name("elasticity_q1_40").scaled(9), P.workloads.CONFIGS[0].scaled(12),
+          P.workloads.CONFIGS[4].scaled(14)):
+    a, b, model = P.workloads.build(w)
+    h.update(P.Precond(a, "ic0").factor().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_ic0_mask_kernel_bit_identical_to_merge_walk():
+    """The mask-driven IC(0) (symbolic masks + mask kernel, per node block on
+    elasticity, per row on Poisson / diffusion) and the merge-walk kernel
+    (PCLAB_IC0_MASKS=0) produce the same factor bits."""
+    outs = []
+    for env in ({"PCLAB_IC0_MASKS": "0"}, {}):
+        e = dict(os.environ, **env)
+        out = subprocess.run([sys.executable, "-c", IC0.format(root=ROOT)], env=e, cwd=ROOT,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stdout + out.stderr
+        outs.append(out.stdout.strip())
+    assert outs[0] == outs[1], outs
