@@ -125,6 +125,92 @@ k_spmv_pap(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict_
     }
 }
 
+// ---- padded p (node-blocked A, bs = 3): p stored as 4 doubles per node
+// (32-byte aligned, pad = 0), so the product gathers a neighbour's three
+// values with ONE 256-bit load instead of three 8-byte loads (a third of
+// the gather wavefronts of the L1-bound product). Entry i lives at
+// 4 (i / 3) + i % 3.
+__device__ __forceinline__ int64_t p4_index(int64_t i) { return 4 * (i / 3) + i % 3; }
+
+__device__ __forceinline__ void ldg256(const double* p, double& a, double& b, double& c, double& d) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+// p <- z + beta p on the padded layout
+__global__ void __launch_bounds__(kT)
+k_pupdate4(int64_t n, const double* __restrict__ z, double* __restrict__ p4, const Scal* S) {
+    if (S->done) return;
+    const double beta = S->beta;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        const int64_t k = p4_index(i);
+        p4[k] = fma(beta, p4[k], z[i]);
+    }
+}
+
+// q = A p (padded p) and pAp: k_spmv_bsr_pap<3> with one 256-bit gather
+// per neighbour block; same per-row summation order.
+__global__ void __launch_bounds__(kT)
+k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+                const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p4,
+                double* __restrict__ q, Scal* S, double* part) {
+    if (S->done) return;
+    constexpr int BS = 3;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * kT) >> 5;
+    double loc = 0.0;
+    BsrRow<BS> m = bsr_row<BS>(gw, nb, rp, bp);
+    for (int64_t b = gw; b < nb; b += nw) {
+        const BsrRow<BS> mn = bsr_row<BS>(b + nw, nb, rp, bp);
+        double acc[BS] = {0.0, 0.0, 0.0};
+        for (int n = lane; n < m.cnt; n += 32) {
+            const int32_t xc = __ldg(bcol + m.c0 + n);
+            double a[BS][BS];
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) a[t][c] = __ldg(vals + m.r[t] + BS * n + c);
+            double xv[4];
+            ldg256(p4 + 4 * static_cast<int64_t>(xc / 3), xv[0], xv[1], xv[2], xv[3]);
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<32>(acc[t]);
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) {
+                const int64_t row = b * BS + t;
+                q[row] = acc[t];
+                loc = fma(p4[4 * b + t], acc[t], loc);
+            }
+        }
+        m = mn;
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
+        S->pap = tot;
+        if (!(tot > 0.0)) {
+            S->error = 1;
+            S->done = 1;
+        } else {
+            S->alpha = S->rz / tot;
+        }
+        S->ctr[0] = 0;
+        S->ctr[1] = 0;
+        S->ctr[2] = 0;
+        S->ctr[3] = 0;
+    }
+}
+
+// x += alpha p (padded p), r -= alpha q, ||r|| -> convergence
+__global__ void __launch_bounds__(kT)
+k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
+        double* __restrict__ r, Scal* S, double* part, double* hist);
+
 // Fused-product variant (Analysis::fused_up): w = A z came out of the
 // backward sweep, so p <- z + beta p, q <- w + beta q (= A p by linearity)
 // and pq in one vector pass; alpha = rz / pq.
@@ -210,6 +296,36 @@ k_axpy(int64_t n, const double* __restrict__ p, const double* __restrict__ q, do
     for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * kT) {
         x[i] = fma(alpha, p[i], x[i]);
+        const double ri = fma(-alpha, q[i], r[i]);
+        r[i] = ri;
+        loc = fma(ri, ri, loc);
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[1], &tot) && threadIdx.x == 0) {
+        S->rr = tot;
+        const double rel = sqrt(tot) / S->bnorm;
+        const long long it = S->iter + 1;
+        S->iter = it;
+        S->rel = rel;
+        if (hist) hist[it] = rel;
+        if (rel <= S->rel_tol) {
+            S->converged = 1;
+            S->done = 1;
+        } else if (it >= S->max_iters) {
+            S->done = 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT)
+k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
+       double* __restrict__ r, Scal* S, double* part, double* hist) {
+    if (S->done) return;
+    const double alpha = S->alpha;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        x[i] = fma(alpha, p4[p4_index(i)], x[i]);
         const double ri = fma(-alpha, q[i], r[i]);
         r[i] = ri;
         loc = fma(ri, ri, loc);
@@ -415,7 +531,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     const int parts_max = sm_count() * 8;
     DevBuf<Scal> S(1);
-    DevBuf<double> part(parts_max), r(n), q(n), pa(n), y, zbuf, wbuf, tmp(n);
+    DevBuf<double> part(parts_max), r(n), q(n), pa, y, zbuf, wbuf, tmp(n);
     DevBuf<double> hist;
     if (record) hist.alloc(max_iters + 1);
     Scal h{};
@@ -453,6 +569,10 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     const Analysis* an = factor ? a.an.get() : nullptr;
     // backward sweep fused with the product (node-blocked matrices)
     const bool fused = an && an->fused_up;
+    // padded p for the node-blocked 3x3 product (PCLAB_PADP=0: plain p)
+    static const bool padp_env = !(getenv("PCLAB_PADP") && atoi(getenv("PCLAB_PADP")) == 0);
+    const bool padp = padp_env && an && an->a_bsr && an->bs == 3 && !fused;
+    pa.alloc(padp ? 4 * (n / 3) : n);
     if (fused) wbuf.alloc(n);
     double* z = r.p;  // kind none: z aliases r
     if (factor) {
@@ -482,7 +602,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         rep.tri_solve_time_per_iter = factor ? tt.ms() / 1e3 : 0.0;
     }
     k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
-    CK(cudaMemsetAsync(pa.p, 0, sizeof(double) * n, st));
+    CK(cudaMemsetAsync(pa.p, 0, pa.bytes(), st));
     CK(cudaMemsetAsync(q.p, 0, sizeof(double) * n, st));  // fused: q <- w + 0 q
     CK_LAUNCH();
     // ---- capture an even number of iterations (p buffers alternate)
@@ -494,6 +614,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     };
     static const unsigned bsr_grid3 = one_wave(k_spmv_bsr_pap<3>);
     static const unsigned bsr_grid2 = one_wave(k_spmv_bsr_pap<2>);
+    static const unsigned bsr_grid4 = one_wave(k_spmv_bsr_pap4);
     // `mark` runs after each of the five kernels (event hook for profiling)
     auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
         if (fused) {
@@ -506,6 +627,24 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             mark();
             launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, &S.p->done, S.p->ctr + 1, st);
             mark();
+            k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+            mark();
+            return;
+        }
+        if (padp) {
+            k_pupdate4<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
+            const BlockCols& bc = an->abc;
+            k_spmv_bsr_pap4<<<bsr_grid4, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p, S.p,
+                                                     part.p);
+            mark();
+            k_axpy4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+            mark();
+            if (factor) {
+                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+                mark();
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+                mark();
+            }
             k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
             mark();
             return;
