@@ -223,7 +223,7 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
 void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
           cudaStream_t st);
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
-                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st);
+                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false);
 // Backward sweep z = U^-1 y fused with w = A z (Analysis::fused_up).
 void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
                        const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,

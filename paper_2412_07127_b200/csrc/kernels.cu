@@ -202,18 +202,33 @@ static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr&
 
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
-template <int LG, int BS, bool UP>
-static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
+template <int LG, int BS, bool UP, bool PAD>
+static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
                          const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
     static unsigned cap = 0;
     if (!cap) {
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP>, BSR_THREADS, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD>, BSR_THREADS, 0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
     const unsigned grid = std::min(trsv_grid(s, 3.0, BSR_THREADS / 32), cap);
-    bsr_trsv_kernel<LG, BS, UP><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b, x, reset,
-                                                              done, trsv_tune(), g_trace);
+    bsr_trsv_kernel<LG, BS, UP, PAD><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b, x,
+                                                                   reset, done, trsv_tune(), g_trace);
+}
+
+// pad: output / re-arm vectors (and the upper sweep's right-hand side)
+// stored 4 doubles per node (PCG loop, BS = 3)
+template <int LG, int BS, bool UP>
+static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, bool pad) {
+    if constexpr (BS == 3) {
+        if (pad) {
+            launch_bsr_p<LG, BS, UP, true>(s, bcol, vals, invd, b, x, reset, done, st);
+            return;
+        }
+    }
+    if (pad) throw DimensionError("padded sweep vectors need 3x3 node blocks");
+    launch_bsr_p<LG, BS, UP, false>(s, bcol, vals, invd, b, x, reset, done, st);
 }
 
 // CTAs given to the fused product (PCLAB_MV_CTAS overrides; default two per SM)
@@ -274,11 +289,11 @@ static void launch_tile_t(const Schedule& s, const double* vals, const double* i
 template <int BS, bool UP>
 static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const BlockCols* bc, const double* vals,
                            const double* invd, const double* b, double* x, double* reset, const int* done,
-                           unsigned* ctr, cudaStream_t st) {
+                           unsigned* ctr, cudaStream_t st, bool pad) {
     if constexpr (BS > 1) {
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
-            if (s.tile.ntiles > 0) {
+            if (s.tile.ntiles > 0 && !pad) {
                 switch (s.lanes) {
                     case 2:
                     case 4: launch_tile_t<4, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
@@ -289,14 +304,14 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
                 return;
             }
             bool chained = false;
-            chained = launch_chain_t<BS, UP>(s, *bc, M, vals, invd, b, x, reset, done, st);
+            if (!pad) chained = launch_chain_t<BS, UP>(s, *bc, M, vals, invd, b, x, reset, done, st);
             if (chained) return;
             switch (s.lanes) {
             case 2:
-            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
-            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
-            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
-            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st); break;
+            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
             }
             return;
         }
@@ -323,19 +338,19 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
 // Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
 // with kPending) and the optional reset buffer.
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool pad) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
-        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
     }
     CK_LAUNCH();
 }

@@ -136,7 +136,9 @@ __device__ __forceinline__ void ldg256(const double* p, double& a, double& b, do
     asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
-// p <- z + beta p on the padded layout
+// p <- z + beta p on the padded layout (ZPAD: z padded too, the sweeps'
+// padded output)
+template <bool ZPAD>
 __global__ void __launch_bounds__(kT)
 k_pupdate4(int64_t n, const double* __restrict__ z, double* __restrict__ p4, const Scal* S) {
     if (S->done) return;
@@ -144,7 +146,7 @@ k_pupdate4(int64_t n, const double* __restrict__ z, double* __restrict__ p4, con
     for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * kT) {
         const int64_t k = p4_index(i);
-        p4[k] = fma(beta, p4[k], z[i]);
+        p4[k] = fma(beta, p4[k], z[ZPAD ? k : i]);
     }
 }
 
@@ -370,6 +372,30 @@ k_dot(int64_t n, const double* __restrict__ a, const double* __restrict__ b, Sca
     }
 }
 
+// k_dot with b on the padded layout (r . z, z the sweeps' padded output)
+// mode 0: rz' -> beta, rz   mode 1: setup rz (beta = 0)   mode 2: bnorm
+__global__ void __launch_bounds__(kT)
+k_dot_z4(int64_t n, const double* __restrict__ a, const double* __restrict__ b, Scal* S, double* part,
+      int mode) {
+    if (mode == 0 && S->done) return;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT)
+        loc = fma(a[i], b[p4_index(i)], loc);
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[2], &tot) && threadIdx.x == 0) {
+        if (mode == 0) {
+            S->beta = tot / S->rz;
+            S->rz = tot;
+        } else if (mode == 1) {
+            S->rz = tot;
+            S->beta = 0.0;
+        } else {
+            S->bnorm = sqrt(tot);
+        }
+    }
+}
+
 __global__ void k_jacobi(int64_t n, const double* __restrict__ r, const double* __restrict__ d,
                          double* __restrict__ z, const Scal* S) {
     if (S->done) return;
@@ -573,14 +599,18 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     static const bool padp_env = !(getenv("PCLAB_PADP") && atoi(getenv("PCLAB_PADP")) == 0);
     const bool padp = padp_env && an && an->a_bsr && an->bs == 3 && !fused;
     pa.alloc(padp ? 4 * (n / 3) : n);
+    // sweep vectors y, z padded too (node-blocked 3x3 sweeps): 256-bit polls
+    // and publications (bsr_item PAD); PCLAB_PADZ=0 keeps them plain
+    static const bool padz_env = !(getenv("PCLAB_PADZ") && atoi(getenv("PCLAB_PADZ")) == 0);
+    const bool padz = padz_env && padp && an->bsr && an->bs == 3;
     if (fused) wbuf.alloc(n);
     double* z = r.p;  // kind none: z aliases r
     if (factor) {
-        y.alloc(n);
-        zbuf.alloc(n);
+        y.alloc(padz ? 4 * (n / 3) : n);
+        zbuf.alloc(padz ? 4 * (n / 3) : n);
         z = zbuf.p;
-        fill_pending(y.p, n, st);
-        fill_pending(z, n, st);
+        fill_pending(y.p, y.n, st);
+        fill_pending(z, zbuf.n, st);
     } else if (pc.kind == Kind::Jacobi) {
         zbuf.alloc(n);
         z = zbuf.p;
@@ -590,18 +620,21 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         Timer tt(st);
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st, padz);
             if (fused)
                 launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, nullptr, S.p->ctr + 1, st);
             else
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st);
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
         CK_LAUNCH();
         rep.tri_solve_time_per_iter = factor ? tt.ms() / 1e3 : 0.0;
     }
-    k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
+    if (padz)
+        k_dot_z4<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
+    else
+        k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
     CK(cudaMemsetAsync(pa.p, 0, pa.bytes(), st));
     CK(cudaMemsetAsync(q.p, 0, sizeof(double) * n, st));  // fused: q <- w + 0 q
     CK_LAUNCH();
@@ -632,7 +665,10 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             return;
         }
         if (padp) {
-            k_pupdate4<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
+            if (padz)
+                k_pupdate4<true><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
+            else
+                k_pupdate4<false><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
             const BlockCols& bc = an->abc;
             k_spmv_bsr_pap4<<<bsr_grid4, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p, S.p,
                                                      part.p);
@@ -640,12 +676,15 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             k_axpy4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
             mark();
             if (factor) {
-                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st, padz);
                 mark();
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st, padz);
                 mark();
             }
-            k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+            if (padz)
+                k_dot_z4<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+            else
+                k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
             mark();
             return;
         }

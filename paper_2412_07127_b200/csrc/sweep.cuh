@@ -420,11 +420,30 @@ __device__ __forceinline__ int slot_nb(const BsrSlot& m) {
 // gl+LG, ...: stream the 3x3 values, poll the neighbours' values, reduce,
 // solve the diagonal block, publish, re-arm `reset`. `flags` = experiment
 // bits of the tune word (see bsr_sweep).
-template <int LG, int BS, bool UPPER>
+//
+// PAD (BS = 3, inside the PCG loop): the sweep's output / re-arm vectors are
+// stored padded, 4 doubles per node, so a dependency poll is ONE 256-bit
+// relaxed load of the neighbour's 3 values and the publication one 256-bit
+// store (a third of the poll instructions and wavefronts); the upper
+// sweep's right-hand side (y) is padded too.
+__device__ __forceinline__ void ld_relaxed_v4(const double* p, double (&v)[3]) {
+    double d;
+    asm volatile("ld.relaxed.gpu.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(d)
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.relaxed.gpu.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+
+template <int LG, int BS, bool UPPER, bool PAD = false>
 __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS], const int32_t* __restrict__ bcol,
                                          const double* __restrict__ vals, const double* __restrict__ invd,
                                          double* out, double* reset, unsigned sleep_ns, int flags, int64_t it,
                                          long long* trace, long long tr0) {
+    static_assert(!PAD || BS == 3, "padded vectors hold 3-dof nodes");
     constexpr int NIB = BS * (BS - 1) / 2;
     const bool exp_vals = flags & 1, exp_nowait = flags & 2, exp_nox = flags & 4;
     const int lane = threadIdx.x & 31;
@@ -468,8 +487,20 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
 #pragma unroll
                 for (int c = 0; c < BS; ++c)
                     a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
+            if constexpr (PAD) {
+                if (exp_nox) {
 #pragma unroll
-            for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
+                    for (int c = 0; c < BS; ++c) xv[c] = 1.0;
+                } else {
+                    double w3[3];
+                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc / 3), w3);
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) xv[c] = w3[c];
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
+            }
             if (exp_nowait)
 #pragma unroll
                 for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
@@ -488,12 +519,27 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
             ++rounds;
             if (sleep_ns) __nanosleep(sleep_ns);
             pend = false;
+            if constexpr (PAD) {
+                bool any = false;
 #pragma unroll
-            for (int c = 0; c < BS; ++c)
-                if (own && is_pending(xv[c])) {
-                    xv[c] = ld_relaxed(out + xc + c);
-                    pend |= is_pending(xv[c]);
+                for (int c = 0; c < BS; ++c) any |= is_pending(xv[c]);
+                if (own && any) {
+                    double w3[3];
+                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc / 3), w3);
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) {
+                        xv[c] = w3[c];
+                        pend |= is_pending(w3[c]);
+                    }
                 }
+            } else {
+#pragma unroll
+                for (int c = 0; c < BS; ++c)
+                    if (own && is_pending(xv[c])) {
+                        xv[c] = ld_relaxed(out + xc + c);
+                        pend |= is_pending(xv[c]);
+                    }
+            }
         }
 #pragma unroll
         for (int t = 0; t < BS; ++t)
@@ -527,8 +573,12 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
                 xb[t] = s * binv[t];
             }
         }
+        if constexpr (PAD) {
+            st_relaxed_v4(out + 4 * static_cast<int64_t>(m.blk), xb[0], xb[1], xb[2], 0.0);
+        } else {
 #pragma unroll
-        for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+        }
     }
     if (trace && lane == 0) {
         long long tr2;
@@ -539,10 +589,10 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
         trace[4LL * it + 3] = min(rounds, 1023);
     }
     __syncwarp();
-    if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+    if (reset && active && gl < BS) reset[(PAD ? 4 * static_cast<int64_t>(m.blk) : r0) + gl] = pending_value();
 }
 
-template <int LG, int BS, bool UPPER>
+template <int LG, int BS, bool UPPER, bool PAD = false>
 __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ srec, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
                                           const double* rhs, double* out, double* reset, int64_t warp,
@@ -552,6 +602,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     // dependency waits, 4 = no dependency loads at all)
     const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
     constexpr int G = 32 / LG;
+    constexpr int RS = PAD && UPPER ? 4 : BS;  // right-hand side stride (padded y)
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     int64_t it = warp;
@@ -562,8 +613,8 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     double rhs0[BS], rhs1[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
-        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
-        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * RS + t] : 0.0;
+        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * RS + t] : 0.0;
     }
     auto prefetch = [&](const BsrSlot& q) {
         if (q.blk >= 0) {
@@ -584,7 +635,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         prefetch(m2);
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
-        bsr_item<LG, BS, UPPER>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0);
+        bsr_item<LG, BS, UPPER, PAD>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0);
         it += nwarps;
         m = m1;
         m1 = m2;
@@ -593,19 +644,19 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
 #pragma unroll
         for (int t = 0; t < BS; ++t) {
             rhs0[t] = rhs1[t];
-            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
+            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * RS + t] : 0.0;
         }
     }
 }
 
-template <int LG, int BS, bool UPPER>
+template <int LG, int BS, bool UPPER, bool PAD>
 __global__ void __launch_bounds__(BSR_THREADS, BSR_CTAS)
 bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                 const double* __restrict__ invd, const double* rhs, double* out, double* reset,
                 const int* __restrict__ done, int tune, long long* trace) {
     if (done && *done) return;
-    bsr_sweep<LG, BS, UPPER>(nitems, srec, bcol, vals, invd, rhs, out, reset,
+    bsr_sweep<LG, BS, UPPER, PAD>(nitems, srec, bcol, vals, invd, rhs, out, reset,
                              (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
                              (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, tune, trace);
 }
