@@ -13,23 +13,45 @@ Per launch, for the layout the kernels actually run on (Precond.layout()):
   pointers, p gathered once, q written;
 * axpy (x += alpha p, r -= alpha q, ||r||): 48 B/row; dot (r.z): 16 B/row.
 
+With 3x3 node blocks the PCG loop keeps p, y and z padded to 4 doubles per
+node (32-byte gathers / polls / publications), so those vectors count
+32/3 B per row where they are read or written.
+
 The reference's own format (scalar CSR, int32 columns, int64 row pointers)
 is reported beside it as `csr_equivalent_bytes`.
 """
 from __future__ import annotations
 
 
-def sweep_bytes(lay: dict, nnz_lower: int, n: int, upper: bool) -> int:
+import os
+
+V4 = 32.0 / 3.0  # bytes per row of a vector padded to 4 doubles per 3-dof node
+
+
+def padded(lay: dict, bs: int, fused: bool = False) -> bool:
+    """Mirror of pcg_solve's choice (pcg.cu): padded p / y / z for 3x3
+    node-blocked A and L outside the fused variant."""
+    env = lambda k: os.environ.get(k, "1") != "0"  # noqa: E731
+    return (lay["a_node_blocked"] and lay["node_blocked"] and bs == 3 and not fused
+            and env("PCLAB_PADP") and env("PCLAB_PADZ"))
+
+
+def sweep_bytes(lay: dict, nnz_lower: int, n: int, upper: bool, pad: bool = False) -> int:
     slots = lay["slots_upper" if upper else "slots_lower"]
     if lay["node_blocked"]:
         bc = lay["block_cols_upper" if upper else "block_cols_lower"]
-        return 8 * nnz_lower + 4 * bc + 16 * slots + 32 * n
+        # rhs (r plain / y padded), 1/l_ii, solution write, re-arm write
+        per_row = (V4 if upper else 8) + 8 + V4 + 8 if pad else 32
+        return int(8 * nnz_lower + 4 * bc + 16 * slots + per_row * n)
     return 12 * nnz_lower + 16 * slots + 32 * n
 
 
-def product_bytes(lay: dict, nnz: int, n: int, bs: int) -> int:
+def product_bytes(lay: dict, nnz: int, n: int, bs: int, pad: bool = False) -> int:
     if lay["a_node_blocked"]:
-        return 24 * n + 8 * nnz + 4 * lay["block_cols_a"] + 8 * n + 8 * (n // bs + 1) + 16 * n
+        v = V4 if pad else 8
+        # p update (z, p read, p written), values, block columns, row and
+        # block pointers, p gathered once, q written
+        return int(3 * v * n + 8 * nnz + 4 * lay["block_cols_a"] + 8 * n + 8 * (n // bs + 1) + (v + 8) * n)
     return 24 * n + 12 * nnz + 8 * (n + 1) + 16 * n
 
 
@@ -49,8 +71,9 @@ def iteration_kernels(pc, n: int, nnz: int, prof: dict) -> dict:
     lay = pc.layout()
     info = pc.info()
     nl, bs = info["nnz_lower"], max(info["block_size"], 1)
-    lo, up = sweep_bytes(lay, nl, n, False), sweep_bytes(lay, nl, n, True)
-    prod = product_bytes(lay, nnz, n, bs)
+    pad = padded(lay, bs, bool(prof.get("fused")))
+    lo, up = sweep_bytes(lay, nl, n, False, pad), sweep_bytes(lay, nl, n, True, pad)
+    prod = product_bytes(lay, nnz, n, bs, pad)
     if prof.get("fused"):
         kern = {
             "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
@@ -63,8 +86,9 @@ def iteration_kernels(pc, n: int, nnz: int, prof: dict) -> dict:
             "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": up},
             "spmv_p": {"ms": prof["spmv_ms"], "bytes": prod},
         }
-    kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": 48 * n}
-    kern["dot"] = {"ms": prof["dot_ms"], "bytes": 16 * n}
+    v = V4 if pad else 8
+    kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": int((v + 40) * n)}  # p, q, x r/w, r r/w
+    kern["dot"] = {"ms": prof["dot_ms"], "bytes": int((8 + v) * n)}
     for k in kern.values():
         k["gbs"] = k["bytes"] / k["ms"] / 1e6 if k["ms"] > 0 else None
     return kern
