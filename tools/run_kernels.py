@@ -1,5 +1,7 @@
 """Developer driver for ncu: build one workload and launch the PCG-loop
-kernels a few times (spmv, both sweeps, one short PCG)."""
+kernels a few times (stand-alone SpMV and both sweeps, then a short IC(0)
+PCG whose loop runs the padded sweeps and the product); with kind 'gnnic'
+also build the GNN-corrected preconditioner once (the GNN kernels)."""
 import os
 import sys
 
@@ -16,7 +18,9 @@ w = P.workloads.by_name(name)
 if m:
     w = w.scaled(m)
 a, b, model = P.workloads.build(w)
-pc = P.Precond(a, kind, model if kind in ("nic", "gnnic") else None)
+pc = P.Precond(a, "ic0")
+if kind in ("nic", "gnnic"):
+    P.Precond(a, kind, model)
 x = torch.randn(a.n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 for _ in range(reps):
@@ -25,9 +29,6 @@ for _ in range(reps):
     pc.trsv_device(True, x.data_ptr(), y.data_ptr())
 bt = torch.from_numpy(b).cuda()
 xt = torch.zeros_like(bt)
-try:
-    rep = pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=1e-8, max_iters=8)
-except P.NumericError as e:  # gnnic on elasticity: the reference's own breakdown
-    rep = {"iterations": str(e)}
+rep = pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=1e-8, max_iters=8)
 torch.cuda.synchronize()
 print("ok", a.n, a.nnz, rep["iterations"])
