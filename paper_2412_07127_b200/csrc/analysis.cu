@@ -257,6 +257,57 @@ __global__ void kahn_persistent(int bs, const int64_t* __restrict__ srp,
     }
 }
 
+// Sync-free levelling over block columns (no grid barrier per level): a
+// work queue of released blocks. A warp pops the next queue slot (waits
+// until it is written), sets level(b) = 1 + max level of its predecessors
+// (all final: a predecessor writes its level, fences, and only then
+// decrements b's counter), fences, and releases the successors whose
+// counters reach zero by appending them. Levels equal Kahn's (longest path
+// from a root). Deadlock-free with every warp resident: slots are written
+// in claim order by running warps, and a popped slot below the number of
+// blocks is always eventually written.
+__global__ void __launch_bounds__(256)
+level_queue_kernel(int64_t nb, int bs, const int64_t* __restrict__ pbp, const int32_t* __restrict__ pbcol,
+                   const int64_t* __restrict__ sbp, const int32_t* __restrict__ sbcol, int32_t* __restrict__ indeg,
+                   int32_t* level, int32_t* queue, unsigned long long* cnt /* [0] head, [1] tail */) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long h = 0;
+        if (lane == 0) h = atomicAdd(cnt, 1ULL);
+        h = __shfl_sync(0xffffffffu, h, 0);
+        if (h >= static_cast<unsigned long long>(nb)) return;
+        int32_t b = -1;
+        if (lane == 0) {
+            volatile int32_t* vq = queue + h;
+            while ((b = *vq) < 0) __nanosleep(32);
+        }
+        b = __shfl_sync(0xffffffffu, b, 0);
+        int lv = 0;
+        for (int64_t k = pbp[b] + lane; k < pbp[b + 1]; k += 32)
+            lv = max(lv, 1 + *reinterpret_cast<volatile int32_t*>(level + pbcol[k] / bs));
+        lv = __reduce_max_sync(0xffffffffu, lv);
+        if (lane == 0) level[b] = lv;
+        __threadfence();
+        __syncwarp();
+        for (int64_t k = sbp[b] + lane; k < sbp[b + 1]; k += 32) {
+            const int64_t jb = sbcol[k] / bs;
+            if (atomicSub(&indeg[jb], 1) == 1) {
+                const unsigned long long t = atomicAdd(cnt + 1, 1ULL);
+                *reinterpret_cast<volatile int32_t*>(queue + t) = static_cast<int32_t>(jb);
+            }
+        }
+    }
+}
+
+__global__ void level_queue_init(int64_t nb, const int64_t* __restrict__ pbp, int32_t* __restrict__ indeg,
+                                 int32_t* __restrict__ queue, unsigned long long* cnt) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nb) return;
+    const int c = static_cast<int>(pbp[b + 1] - pbp[b]);
+    indeg[b] = c;
+    if (c == 0) queue[atomicAdd(cnt + 1, 1ULL)] = static_cast<int32_t>(b);
+}
+
 __global__ void kahn_start(KState* ks) {
     ks->beg = 0;
     ks->end = ks->tail;
@@ -485,6 +536,32 @@ void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, 
     if (s.nblocks == 0) return;
     const int64_t nb = s.nblocks;
     const bool bc = pbc && sbc && pbc->bp.p && sbc->bp.p;
+    static const bool queue_on = !(getenv("PCLAB_LEVEL_QUEUE") && atoi(getenv("PCLAB_LEVEL_QUEUE")) == 0);
+    if (bc && queue_on) {
+        DevBuf<int32_t> indeg(nb), queue(nb);
+        DevBuf<unsigned long long> cnt(2);
+        CK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(queue.p, 0xff, sizeof(int32_t) * nb, st));
+        level_queue_init<<<grid_for(nb, 256), 256, 0, st>>>(nb, pbc->bp.p, indeg.p, queue.p, cnt.p);
+        CK_LAUNCH();
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_queue_kernel, 256, 0));
+        const unsigned grid = static_cast<unsigned>(sm_count() * std::max(1, std::min(per_sm, 4)));
+        level_queue_kernel<<<grid, 256, 0, st>>>(nb, bs, pbc->bp.p, pbc->bcol.p, sbc->bp.p, sbc->bcol.p, indeg.p,
+                                                 s.level.p, queue.p, cnt.p);
+        CK_LAUNCH();
+        unsigned long long hc[2];
+        CK(cudaMemcpyAsync(hc, cnt.p, sizeof hc, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hc[1] != static_cast<unsigned long long>(nb))
+            throw FormatError("level analysis: dependency graph has a cycle");
+        if (s.need_crit) {
+            crit_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, pred.rp.p, pred.cols.p, upper, s.level.p,
+                                                           s.crit.p);
+            CK_LAUNCH();
+        }
+        return;
+    }
     DevBuf<int32_t> indeg(nb), fr(nb);
     DevBuf<KState> ks(1);
     CK(cudaMemsetAsync(ks.p, 0, sizeof(KState), st));
