@@ -475,76 +475,97 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
     for (int t = 0; t < BS; ++t) acc[t] = 0.0;
     const int nbmax = __reduce_max_sync(0xffffffffu, nb);
     int rounds = 0;
-    for (int n0 = 0; n0 < nbmax; n0 += LG) {
-        const int n = n0 + gl;
-        const bool own = n < nb;
-        double a[BS][BS], xv[BS];
-        int32_t xc = 0;
-        if (own) {
-            xc = ld_stream(bcol + m.bp + n);
+    // RU neighbour rounds per pass with every load of the pass issued
+    // before the first poll (LG = 8: a lane owns neighbours gl and gl + 8)
+    constexpr int RU = LG <= 8 ? 2 : 1;
+    for (int n0 = 0; n0 < nbmax; n0 += LG * RU) {
+        double a[RU][BS][BS], xv[RU][BS];
+        int32_t xc[RU];
+        bool own[RU];
 #pragma unroll
-            for (int t = 0; t < BS; ++t)
+        for (int r = 0; r < RU; ++r) {
+            const int n = n0 + r * LG + gl;
+            own[r] = n < nb;
+            xc[r] = 0;
+            if (own[r]) {
+                xc[r] = ld_stream(bcol + m.bp + n);
 #pragma unroll
-                for (int c = 0; c < BS; ++c)
-                    a[t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
-            if constexpr (PAD) {
-                if (exp_nox) {
+                for (int t = 0; t < BS; ++t)
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[c] = 1.0;
-                } else {
-                    double w3[3];
-                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc / 3), w3);
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[c] = w3[c];
-                }
+                    for (int c = 0; c < BS; ++c)
+                        a[r][t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
             } else {
 #pragma unroll
-                for (int c = 0; c < BS; ++c) xv[c] = exp_nox ? 1.0 : ld_relaxed(out + xc + c);
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) a[r][t][c] = 0.0;
             }
-            if (exp_nowait)
+        }
 #pragma unroll
-                for (int c = 0; c < BS; ++c) xv[c] = is_pending(xv[c]) ? 0.0 : xv[c];
-        } else {
+        for (int r = 0; r < RU; ++r) {
+            if (own[r]) {
+                if constexpr (PAD) {
+                    if (exp_nox) {
 #pragma unroll
-            for (int t = 0; t < BS; ++t) {
-                xv[t] = 0.0;
+                        for (int c = 0; c < BS; ++c) xv[r][c] = 1.0;
+                    } else {
+                        double w3[3];
+                        ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc[r] / 3), w3);
 #pragma unroll
-                for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
+                        for (int c = 0; c < BS; ++c) xv[r][c] = w3[c];
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) xv[r][c] = exp_nox ? 1.0 : ld_relaxed(out + xc[r] + c);
+                }
+                if (exp_nowait)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) xv[r][c] = is_pending(xv[r][c]) ? 0.0 : xv[r][c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < BS; ++c) xv[r][c] = 0.0;
             }
         }
         bool pend = false;
 #pragma unroll
-        for (int c = 0; c < BS; ++c) pend |= own && is_pending(xv[c]);
+        for (int r = 0; r < RU; ++r)
+#pragma unroll
+            for (int c = 0; c < BS; ++c) pend |= own[r] && is_pending(xv[r][c]);
         while (__any_sync(0xffffffffu, pend)) {
             ++rounds;
             if (sleep_ns) __nanosleep(sleep_ns);
             pend = false;
-            if constexpr (PAD) {
-                bool any = false;
 #pragma unroll
-                for (int c = 0; c < BS; ++c) any |= is_pending(xv[c]);
-                if (own && any) {
-                    double w3[3];
-                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc / 3), w3);
+            for (int r = 0; r < RU; ++r) {
+                if constexpr (PAD) {
+                    bool any = false;
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) {
-                        xv[c] = w3[c];
-                        pend |= is_pending(w3[c]);
+                    for (int c = 0; c < BS; ++c) any |= is_pending(xv[r][c]);
+                    if (own[r] && any) {
+                        double w3[3];
+                        ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc[r] / 3), w3);
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) {
+                            xv[r][c] = w3[c];
+                            pend |= is_pending(w3[c]);
+                        }
                     }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BS; ++c)
+                        if (own[r] && is_pending(xv[r][c])) {
+                            xv[r][c] = ld_relaxed(out + xc[r] + c);
+                            pend |= is_pending(xv[r][c]);
+                        }
                 }
-            } else {
-#pragma unroll
-                for (int c = 0; c < BS; ++c)
-                    if (own && is_pending(xv[c])) {
-                        xv[c] = ld_relaxed(out + xc + c);
-                        pend |= is_pending(xv[c]);
-                    }
             }
         }
 #pragma unroll
-        for (int t = 0; t < BS; ++t)
+        for (int r = 0; r < RU; ++r)
 #pragma unroll
-            for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[t] = fma(a[r][t][c], xv[r][c], acc[t]);
     }
     long long trg = 0;
     if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
