@@ -152,7 +152,10 @@ k_pupdate4(int64_t n, const double* __restrict__ z, double* __restrict__ p4, con
 
 // q = A p (padded p) and pAp: k_spmv_bsr_pap<3> with one 256-bit gather
 // per neighbour block; same per-row summation order.
-__global__ void __launch_bounds__(kT)
+#ifndef PAP4_MINB
+#define PAP4_MINB 4
+#endif
+__global__ void __launch_bounds__(kT, PAP4_MINB)
 k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p4,
                 double* __restrict__ q, Scal* S, double* part) {

@@ -432,6 +432,7 @@ __device__ __forceinline__ void ld_relaxed_v4(const double* p, double (&v)[3]) {
                  : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(d)
                  : "l"(p)
                  : "memory");
+    (void)d;  // the pad element
 }
 __device__ __forceinline__ void st_relaxed_v4(double* p, double a, double b, double c, double d) {
     asm volatile("st.relaxed.gpu.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
