@@ -40,6 +40,10 @@ def parse():
     ap.add_argument("--kind", default="ic0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=2, help="PCG iterations per reference step")
+    ap.add_argument("--bw-elasticity", action="store_true",
+                    help="per-kernel bandwidth of SpMV / both node-blocked sweeps on configs[2] (5.0M dofs) and "
+                         "configs[3] (10.1M dofs); configs[3]'s IC(0) breaks down like the reference's, so its "
+                         "sweeps run on the NIC factor (timing does not depend on the values)")
     ap.add_argument("--bw-sweep", action="store_true",
                     help="BASELINE configs[4]: per-kernel bandwidth of SpMV / both sweeps at 64^3, 128^3, "
                          "256^3 and the IC(0)+GNN PCG solve at each size (one JSON line per size)")
@@ -399,8 +403,63 @@ def run_bw_sweep(args):
         del pc, pc2, a
 
 
+def run_bw_elasticity(args):
+    import torch
+    import paper_2412_07127_b200 as P
+    from paper_2412_07127_b200 import traffic as T
+    import paper_2412_07127_b200.workloads as WL
+
+    torch.cuda.set_device(0)
+    hbm, peak_kind = peaks()
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    for name in ("elasticity_q1_118", "elasticity_q1_149"):
+        w = WL.by_name(name)
+        a, b_host, model = WL.build(w)
+        n, _, nnz = a.shape()
+        try:
+            pc, factor = P.Precond(a, "ic0"), "ic0"
+        except P.NumericError as e:
+            pc, factor = P.Precond(a, "nic", model), f"nic (ic0: {e})"
+        lay, info = pc.layout(), pc.info()
+        x = torch.randn(n, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+
+        def timed(f, reps=10):
+            ts = []
+            for _ in range(reps + 2):
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                f()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return float(np.median(ts[2:]))
+
+        bs = max(info["block_size"], 1)
+        ks = {
+            "spmv": (timed(lambda: a.spmv_device(x.data_ptr(), y.data_ptr())), T.spmv_bytes(lay, nnz, n, bs)),
+            "sweep_lower": (timed(lambda: pc.trsv_device(False, x.data_ptr(), y.data_ptr())),
+                            T.sweep_bytes(lay, info["nnz_lower"], n, False)),
+            "sweep_upper": (timed(lambda: pc.trsv_device(True, x.data_ptr(), y.data_ptr())),
+                            T.sweep_bytes(lay, info["nnz_lower"], n, True)),
+        }
+        kern = {k: {"ms": v[0], "bytes": v[1], "gbs": v[1] / v[0] / 1e6, "frac": v[1] / v[0] / 1e6 / hbm}
+                for k, v in ks.items()}
+        print(json.dumps({
+            "metric": "kernel_bandwidth", "workload": w.name, "n": n, "nnz": nnz, "factor": factor,
+            "levels": [info["block_levels_lower"], info["block_levels_upper"]], "peak_gbs": hbm,
+            "peak_source": peak_kind, "l2": "flushed before every launch",
+            "note": "stand-alone kernels on plain vectors (the PCG loop runs the padded-vector variants)",
+            "kernels": kern}), flush=True)
+        del pc, a
+
+
 def main():
     args = parse()
+    if args.bw_elasticity:
+        run_bw_elasticity(args)
+        return
     if args.bw_sweep:
         run_bw_sweep(args)
         return

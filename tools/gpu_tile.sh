@@ -1,3 +1,1 @@
-for env in "PCLAB_X=1" "PCLAB_LIB=build/var/libpclab_pap5.so"; do
-  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/pap5.log 2>&1
-done
+timeout 900 python bench.py --bw-elasticity > gpurun_out/bwe.log 2> gpurun_out/bwe.err
