@@ -222,8 +222,10 @@ void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* ou
 void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
 void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
           cudaStream_t st);
+struct RUpdate;  // sweep.cuh: forward sweep fused with r_new = r - alpha q
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
-                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false);
+                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false,
+                 const RUpdate* ru = nullptr);
 // Backward sweep z = U^-1 y fused with w = A z (Analysis::fused_up).
 void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
                        const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,

@@ -202,33 +202,41 @@ static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr&
 
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
-template <int LG, int BS, bool UP, bool PAD>
+template <int LG, int BS, bool UP, bool PAD, bool RAX>
 static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, RUpdate ru) {
     static unsigned cap = 0;
     if (!cap) {
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD>, BSR_THREADS, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD, RAX>, BSR_THREADS,
+                                                         0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
     const unsigned grid = std::min(trsv_grid(s, 3.0, BSR_THREADS / 32), cap);
-    bsr_trsv_kernel<LG, BS, UP, PAD><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b, x,
-                                                                   reset, done, trsv_tune(), g_trace);
+    bsr_trsv_kernel<LG, BS, UP, PAD, RAX><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b,
+                                                                        x, reset, done, trsv_tune(), g_trace, ru);
 }
 
 // pad: output / re-arm vectors (and the upper sweep's right-hand side)
-// stored 4 doubles per node (PCG loop, BS = 3)
+// stored 4 doubles per node (PCG loop, BS = 3); ru: forward sweep fused
+// with r_new = r - alpha q (PCG loop, padded)
 template <int LG, int BS, bool UP>
 static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, bool pad) {
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, bool pad,
+                         const RUpdate* ru) {
     if constexpr (BS == 3) {
-        if (pad) {
-            launch_bsr_p<LG, BS, UP, true>(s, bcol, vals, invd, b, x, reset, done, st);
+        if (pad && ru) {
+            if constexpr (!UP) {
+                launch_bsr_p<LG, BS, UP, true, true>(s, bcol, vals, invd, b, x, reset, done, st, *ru);
+                return;
+            }
+        } else if (pad) {
+            launch_bsr_p<LG, BS, UP, true, false>(s, bcol, vals, invd, b, x, reset, done, st, RUpdate{});
             return;
         }
     }
-    if (pad) throw DimensionError("padded sweep vectors need 3x3 node blocks");
-    launch_bsr_p<LG, BS, UP, false>(s, bcol, vals, invd, b, x, reset, done, st);
+    if (pad || ru) throw DimensionError("padded / fused-residual sweeps need 3x3 node blocks (forward sweep)");
+    launch_bsr_p<LG, BS, UP, false, false>(s, bcol, vals, invd, b, x, reset, done, st, RUpdate{});
 }
 
 // CTAs given to the fused product (PCLAB_MV_CTAS overrides; default two per SM)
@@ -289,11 +297,12 @@ static void launch_tile_t(const Schedule& s, const double* vals, const double* i
 template <int BS, bool UP>
 static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const BlockCols* bc, const double* vals,
                            const double* invd, const double* b, double* x, double* reset, const int* done,
-                           unsigned* ctr, cudaStream_t st, bool pad) {
+                           unsigned* ctr, cudaStream_t st, bool pad, const RUpdate* ru) {
+    if ((pad || ru) && !bc) throw DimensionError("padded / fused-residual sweeps need the node-blocked sweep");
     if constexpr (BS > 1) {
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
-            if (s.tile.ntiles > 0 && !pad) {
+            if (s.tile.ntiles > 0 && !pad && !ru) {
                 switch (s.lanes) {
                     case 2:
                     case 4: launch_tile_t<4, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
@@ -308,10 +317,10 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
             if (chained) return;
             switch (s.lanes) {
             case 2:
-            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
-            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
-            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
-            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
+            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
             }
             return;
         }
@@ -338,19 +347,19 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
 // Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
 // with kPending) and the optional reset buffer.
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                 cudaStream_t st, bool pad) {
+                 cudaStream_t st, bool pad, const RUpdate* ru) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
-        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
+        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
-        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
+        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
     }
     CK_LAUNCH();
 }

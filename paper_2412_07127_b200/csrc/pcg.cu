@@ -31,7 +31,11 @@ constexpr int kT = 256;
 struct Scal {
     double rz, pap, alpha, beta, bnorm, rel, rel_tol, rr;
     long long iter, max_iters;
-    int done, converged, error, pad;
+    // done_sweep: the done flag as of the product, read by the sweeps of the
+    // fused-residual loop -- the concurrent x / ||r|| kernel may raise `done`
+    // while a sweep's CTAs are starting, and a sweep whose CTAs disagree on it
+    // would leave items unprocessed
+    int done, converged, error, done_sweep;
     unsigned ticket[4];
     unsigned ctr[4];  // sweep L items, sweep U items, fused CTA roles, product pairs
 };
@@ -159,7 +163,10 @@ __global__ void __launch_bounds__(kT, PAP4_MINB)
 k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p4,
                 double* __restrict__ q, Scal* S, double* part) {
-    if (S->done) return;
+    if (S->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) S->done_sweep = 1;
+        return;
+    }
     constexpr int BS = 3;
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
@@ -204,6 +211,7 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
         } else {
             S->alpha = S->rz / tot;
         }
+        S->done_sweep = S->done;
         S->ctr[0] = 0;
         S->ctr[1] = 0;
         S->ctr[2] = 0;
@@ -215,6 +223,13 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
 __global__ void __launch_bounds__(kT)
 k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
         double* __restrict__ r, Scal* S, double* part, double* hist);
+
+// x += alpha p (padded p) and ||r - alpha q|| -> convergence, r not written:
+// runs concurrently with the forward sweep that forms and stores r_new
+// itself (RUpdate); own partials buffer (the dot may overlap it)
+__global__ void __launch_bounds__(kT)
+k_xrr4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
+       const double* __restrict__ r, Scal* S, double* part, double* hist);
 
 // Fused-product variant (Analysis::fused_up): w = A z came out of the
 // backward sweep, so p <- z + beta p, q <- w + beta q (= A p by linearity)
@@ -333,6 +348,35 @@ k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, 
         x[i] = fma(alpha, p4[p4_index(i)], x[i]);
         const double ri = fma(-alpha, q[i], r[i]);
         r[i] = ri;
+        loc = fma(ri, ri, loc);
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[1], &tot) && threadIdx.x == 0) {
+        S->rr = tot;
+        const double rel = sqrt(tot) / S->bnorm;
+        const long long it = S->iter + 1;
+        S->iter = it;
+        S->rel = rel;
+        if (hist) hist[it] = rel;
+        if (rel <= S->rel_tol) {
+            S->converged = 1;
+            S->done = 1;
+        } else if (it >= S->max_iters) {
+            S->done = 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT)
+k_xrr4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
+       const double* __restrict__ r, Scal* S, double* part, double* hist) {
+    if (S->done) return;
+    const double alpha = S->alpha;
+    double loc = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        x[i] = fma(alpha, p4[p4_index(i)], x[i]);
+        const double ri = fma(-alpha, q[i], r[i]);
         loc = fma(ri, ri, loc);
     }
     double tot;
@@ -651,6 +695,34 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     static const unsigned bsr_grid3 = one_wave(k_spmv_bsr_pap<3>);
     static const unsigned bsr_grid2 = one_wave(k_spmv_bsr_pap<2>);
     static const unsigned bsr_grid4 = one_wave(k_spmv_bsr_pap4);
+    // forward sweep fused with the residual update, x / ||r|| on a side
+    // stream (padded node-blocked loop). Opt-in (PCLAB_RAX=1): on configs[2]
+    // the loop gains ~9 us per iteration (k_axpy4 hidden, the forward sweep
+    // 25 us slower with the extra q load / r store) -- within run-to-run noise
+    static const bool rax_env = getenv("PCLAB_RAX") && atoi(getenv("PCLAB_RAX")) != 0;
+    const bool rax = rax_env && padz;
+    DevBuf<double> r2, part2;
+    if (rax) {
+        r2.alloc(n);
+        part2.alloc(parts_max);
+    }
+    int rpar = 0;            // residual buffer parity (r, r2 alternate)
+    bool seq_side = false;   // profiling: the side kernel runs in order
+    bool side_pending = false;
+    static thread_local cudaStream_t side = [] {
+        cudaStream_t t;
+        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+        return t;
+    }();
+    cudaEvent_t ev_fork, ev_join;
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    auto join_side = [&] {
+        if (side_pending) {
+            CK(cudaStreamWaitEvent(st, ev_join, 0));
+            side_pending = false;
+        }
+    };
     // `mark` runs after each of the five kernels (event hook for profiling)
     auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
         if (fused) {
@@ -668,6 +740,10 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             return;
         }
         if (padp) {
+            if (side_pending) {  // the previous iteration's x update read p
+                CK(cudaStreamWaitEvent(st, ev_join, 0));
+                side_pending = false;
+            }
             if (padz)
                 k_pupdate4<true><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
             else
@@ -676,6 +752,36 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             k_spmv_bsr_pap4<<<bsr_grid4, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p, S.p,
                                                      part.p);
             mark();
+            if (rax) {
+                // r_new = r - alpha q is formed by the forward sweep itself; x
+                // and ||r_new|| on a side stream, concurrent with the sweeps
+                // (joined before the next p update, which overwrites p)
+                double* rold = rpar ? r2.p : r.p;
+                double* rnew = rpar ? r.p : r2.p;
+                rpar ^= 1;
+                if (seq_side) {
+                    k_xrr4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, rold, S.p, part2.p, record ? hist.p : nullptr);
+                } else {
+                    CK(cudaEventRecord(ev_fork, st));
+                    CK(cudaStreamWaitEvent(side, ev_fork, 0));
+                    k_xrr4<<<vgrid, kT, 0, side>>>(n, pp, q.p, x, rold, S.p, part2.p, record ? hist.p : nullptr);
+                    CK(cudaEventRecord(ev_join, side));
+                    side_pending = true;
+                }
+                mark();
+                RUpdate ru;
+                ru.q = q.p;
+                ru.rnew = rnew;
+                ru.alpha = &S.p->alpha;
+                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, rold, y.p, z, &S.p->done_sweep, S.p->ctr, st, true,
+                            &ru);
+                mark();
+                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done_sweep, S.p->ctr + 1, st, true);
+                mark();
+                k_dot_z4<<<vgrid, kT, 0, st>>>(n, rnew, z, S.p, part.p, 0);
+                mark();
+                return;
+            }
             k_axpy4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
             mark();
             if (factor) {
@@ -733,6 +839,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     int* hdone = nullptr;
     CK(cudaMallocHost(&hdone, sizeof(int)));
     if (prof_ms) {
+        seq_side = true;  // the side kernel in stream order: its own slot
         // eager iterations with an event between kernels: per-kernel device
         // times averaged over iterations, [spmv_p, axpy, sweep L, sweep U,
         // dot] or, fused, [pq, axpy, sweep L, sweep U + A z, dot]
@@ -766,6 +873,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         // developer knob: stream-launched iterations, done flag read every 8
         for (;;) {
             for (int k = 0; k < 8; ++k) iteration(pa.p, nullptr);
+            join_side();
             CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             if (*hdone) break;
@@ -781,6 +889,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             iteration(pa.p, nullptr);
             iteration(pa.p, nullptr);
         }
+        join_side();  // the side stream rejoins before the capture ends
         CK(cudaStreamEndCapture(st, &graph));
         CK(cudaGraphInstantiate(&exec, graph, 0));
         size_t nodes = 0;
@@ -801,6 +910,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         cudaGraphExecDestroy(exec);
         cudaGraphDestroy(graph);
     }
+    join_side();
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
     cudaFreeHost(hdone);
     rep.cg_time = cg.ms() / 1e3;
     CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));

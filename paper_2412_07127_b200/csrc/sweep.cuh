@@ -415,6 +415,16 @@ __device__ __forceinline__ int slot_nb(const BsrSlot& m) {
 // and every load is issued a whole item before its value is needed:
 //   item k+3: slot record        item k+2: entries prefetched into L1
 //   item k+1: right-hand side    item k:   entries, dependency polls
+// Forward sweep fused with the residual update (PCG loop, RAX): the
+// right-hand side of block b is r_new = r - alpha q, computed as it is
+// loaded (the fma k_axpy uses) and written to `rnew` by the group's lane 0;
+// x and ||r_new|| are updated by a concurrent kernel.
+struct RUpdate {
+    const double* q = nullptr;
+    double* rnew = nullptr;
+    const double* alpha = nullptr;
+};
+
 // One item of the node-blocked sweep: this lane group's block `m` (rows
 // r0..r0+BS-1, right-hand side rc), lane gl owning neighbour blocks gl,
 // gl+LG, ...: stream the 3x3 values, poll the neighbours' values, reduce,
@@ -439,11 +449,11 @@ __device__ __forceinline__ void st_relaxed_v4(double* p, double a, double b, dou
                  : "memory");
 }
 
-template <int LG, int BS, bool UPPER, bool PAD = false>
+template <int LG, int BS, bool UPPER, bool PAD = false, bool RAX = false>
 __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS], const int32_t* __restrict__ bcol,
                                          const double* __restrict__ vals, const double* __restrict__ invd,
                                          double* out, double* reset, unsigned sleep_ns, int flags, int64_t it,
-                                         long long* trace, long long tr0) {
+                                         long long* trace, long long tr0, double* rnew = nullptr) {
     static_assert(!PAD || BS == 3, "padded vectors hold 3-dof nodes");
     constexpr int NIB = BS * (BS - 1) / 2;
     const bool exp_vals = flags & 1, exp_nowait = flags & 2, exp_nox = flags & 4;
@@ -595,6 +605,10 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
                 xb[t] = s * binv[t];
             }
         }
+        if constexpr (RAX) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) rnew[r0 + t] = rc[t];
+        }
         if constexpr (PAD) {
             st_relaxed_v4(out + 4 * static_cast<int64_t>(m.blk), xb[0], xb[1], xb[2], 0.0);
         } else {
@@ -614,17 +628,20 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
     if (reset && active && gl < BS) reset[(PAD ? 4 * static_cast<int64_t>(m.blk) : r0) + gl] = pending_value();
 }
 
-template <int LG, int BS, bool UPPER, bool PAD = false>
+template <int LG, int BS, bool UPPER, bool PAD = false, bool RAX = false>
 __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ srec, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
                                           const double* rhs, double* out, double* reset, int64_t warp,
-                                          int64_t nwarps, int tune, long long* trace) {
+                                          int64_t nwarps, int tune, long long* trace, RUpdate ru = RUpdate{}) {
     // tune: sleep_ns << 8 | experiment bits (developer timing probes that
     // give WRONG results: 1 = matrix values from one cached line, 2 = no
     // dependency waits, 4 = no dependency loads at all)
     const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
     constexpr int G = 32 / LG;
     constexpr int RS = PAD && UPPER ? 4 : BS;  // right-hand side stride (padded y)
+    const double alpha = RAX ? *ru.alpha : 0.0;
+    // right-hand side entry i (RAX: r_new = r - alpha q, as k_axpy forms it)
+    auto rhs_at = [&](int64_t i) { return RAX ? fma(-alpha, ru.q[i], rhs[i]) : rhs[i]; };
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     int64_t it = warp;
@@ -635,8 +652,8 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     double rhs0[BS], rhs1[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
-        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * RS + t] : 0.0;
-        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * RS + t] : 0.0;
+        rhs0[t] = m.blk >= 0 ? rhs_at(static_cast<int64_t>(m.blk) * RS + t) : 0.0;
+        rhs1[t] = m1.blk >= 0 ? rhs_at(static_cast<int64_t>(m1.blk) * RS + t) : 0.0;
     }
     auto prefetch = [&](const BsrSlot& q) {
         if (q.blk >= 0) {
@@ -657,7 +674,8 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         prefetch(m2);
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
-        bsr_item<LG, BS, UPPER, PAD>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0);
+        bsr_item<LG, BS, UPPER, PAD, RAX>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0,
+                                          ru.rnew);
         it += nwarps;
         m = m1;
         m1 = m2;
@@ -666,21 +684,21 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
 #pragma unroll
         for (int t = 0; t < BS; ++t) {
             rhs0[t] = rhs1[t];
-            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * RS + t] : 0.0;
+            rhs1[t] = m1.blk >= 0 ? rhs_at(static_cast<int64_t>(m1.blk) * RS + t) : 0.0;
         }
     }
 }
 
-template <int LG, int BS, bool UPPER, bool PAD>
+template <int LG, int BS, bool UPPER, bool PAD, bool RAX = false>
 __global__ void __launch_bounds__(BSR_THREADS, BSR_CTAS)
 bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                 const double* __restrict__ invd, const double* rhs, double* out, double* reset,
-                const int* __restrict__ done, int tune, long long* trace) {
+                const int* __restrict__ done, int tune, long long* trace, RUpdate ru) {
     if (done && *done) return;
-    bsr_sweep<LG, BS, UPPER, PAD>(nitems, srec, bcol, vals, invd, rhs, out, reset,
-                             (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
-                             (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, tune, trace);
+    bsr_sweep<LG, BS, UPPER, PAD, RAX>(nitems, srec, bcol, vals, invd, rhs, out, reset,
+                                       (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                                       (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, tune, trace, ru);
 }
 
 // ------------------------------------------------------------------------

@@ -2,8 +2,10 @@
 per process): the backward sweep fused with the product (PCLAB_FUSE=1),
 the chain-segment sweep (PCLAB_CHAIN=1), the entry-lane sweep on a
 node-blocked matrix (PCLAB_BSR=0), the round-robin node-blocked sweep
-(PCLAB_TILE=0) and the tiled sweep under few tiles / many pieces / a
-64-slot ring (recycled slots take the L2 path). Same parity bar as the
+(PCLAB_TILE=0), the tiled sweep under few tiles / many pieces / a
+64-slot ring (recycled slots take the L2 path), the forward sweep fused with
+the residual update and x / ||r|| on a side stream (PCLAB_RAX=1), and the
+unpadded p / y / z vectors (PCLAB_PADZ=0, PCLAB_PADP=0). Same parity bar as the
 default path: PCG iterations +-1 and the solution within 1e-8 of the
 oracle, sweeps within 1e-12."""
 import os
@@ -46,7 +48,8 @@ print("ok", rep["iterations"], ro["iterations"])
 
 @pytest.mark.parametrize("env", [{"PCLAB_FUSE": "1"}, {"PCLAB_CHAIN": "1"}, {"PCLAB_BSR": "0"},
                                  {"PCLAB_CHAIN": "1", "PCLAB_CHAIN_K": "3"}, {"PCLAB_TILE": "0"},
-                                 {"PCLAB_TILES": "3", "PCLAB_TILE_K": "4"}, {"PCLAB_TILE_RING": "64"}])
+                                 {"PCLAB_TILES": "3", "PCLAB_TILE_K": "4"}, {"PCLAB_TILE_RING": "64"},
+                                 {"PCLAB_RAX": "1"}, {"PCLAB_PADZ": "0"}, {"PCLAB_PADP": "0"}])
 def test_variant_parity(env):
     e = dict(os.environ, **env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=e, cwd=ROOT,
