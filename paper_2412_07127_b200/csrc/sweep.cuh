@@ -348,24 +348,6 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-// 16-byte asynchronous global -> shared copy (LDGSTS), evict-first in L2
-// like ld_stream: the matrix stream is read once per sweep.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile(
-        "{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
-        "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n\t}" ::"r"(smem_addr(dst)),
-        "l"(src)
-        : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// doubles of one block's staged rows (node-blocked sweep): 3 elasticity
-// rows of <= 42 entries, 16-byte aligned
-constexpr int kStageD = 128;
-constexpr int kStages = 3;
 
 // Per-item state of the node-blocked sweep: one 16-byte slot record
 // (Schedule::slot_rp) = {block (-1: idle lane group), first row pointer,

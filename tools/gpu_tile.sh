@@ -1,4 +1,3 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/tall2.log 2>&1; echo RC $? >> gpurun_out/tall2.log
-for env in "PCLAB_RAX=1" "PCLAB_RAX=0"; do
-  env $env timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/brax2_$env.log 2>&1
+for t in 0 6400 12800 25600 51200; do
+  PCLAB_TRSV_TUNE=$t timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/sleep.log 2>&1
 done
