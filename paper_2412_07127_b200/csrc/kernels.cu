@@ -212,7 +212,7 @@ static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* v
                                                          0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
-    const unsigned grid = std::min(trsv_grid(s, 3.0, BSR_THREADS / 32), cap);
+    const unsigned grid = std::min(trsv_grid(s, 4.0, BSR_THREADS / 32), cap);  // ~all resident warps
     bsr_trsv_kernel<LG, BS, UP, PAD, RAX><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b,
                                                                         x, reset, done, trsv_tune(), g_trace, ru);
 }

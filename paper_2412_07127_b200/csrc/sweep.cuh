@@ -13,13 +13,14 @@
 #ifndef BSR_MINB
 #define BSR_MINB 2
 #endif
-// node-blocked sweep CTA: 128 threads, 5 resident per SM (20 warps within
-// the register file at <= 102 registers per thread)
+// node-blocked sweep CTA: 128 threads, 6 resident per SM (24 warps at <= 80
+// registers per thread; a few bytes of spill). Measured on configs[2]
+// (per sweep): 5/SM 0.934 ms, 6/SM 0.904, 7/SM 1.02, 8/SM 1.09 (spills)
 #ifndef BSR_THREADS
 #define BSR_THREADS 128
 #endif
 #ifndef BSR_CTAS
-#define BSR_CTAS 5
+#define BSR_CTAS 6
 #endif
 
 

@@ -1,3 +1,2 @@
-for t in 0 6400 12800 25600 51200; do
-  PCLAB_TRSV_TUNE=$t timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/sleep.log 2>&1
-done
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/tall3.log 2>&1; echo RC $? >> gpurun_out/tall3.log
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b6.log 2>&1
