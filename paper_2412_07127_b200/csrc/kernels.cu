@@ -202,19 +202,29 @@ static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr&
 
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
-template <int LG, int BS, bool UP, bool PAD, bool RAX>
-static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
+template <int LG, int BS, bool UP, bool PAD, bool RAX, bool DEV>
+static void launch_bsr_d(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
                          const double* b, double* x, double* reset, const int* done, cudaStream_t st, RUpdate ru) {
     static unsigned cap = 0;
     if (!cap) {
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD, RAX>, BSR_THREADS,
-                                                         0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD, RAX, DEV>,
+                                                         BSR_THREADS, 0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
-    const unsigned grid = std::min(trsv_grid(s, 4.0, BSR_THREADS / 32), cap);  // ~all resident warps
-    bsr_trsv_kernel<LG, BS, UP, PAD, RAX><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b,
-                                                                        x, reset, done, trsv_tune(), g_trace, ru);
+    const unsigned grid = std::min(trsv_grid(s, 5.0, BSR_THREADS / 32), cap);  // ~all resident warps
+    bsr_trsv_kernel<LG, BS, UP, PAD, RAX, DEV><<<grid, BSR_THREADS, 0, st>>>(
+        s.nitems, s.slot_rp.p, bcol, vals, invd, b, x, reset, done, trsv_tune(), g_trace, ru);
+}
+
+// developer probes (PCLAB_TRSV_TUNE, PCLAB_TRSV_TRACE) select the DEV build
+template <int LG, int BS, bool UP, bool PAD, bool RAX>
+static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, RUpdate ru) {
+    if (trsv_tune() != 0 || g_trace != nullptr)
+        launch_bsr_d<LG, BS, UP, PAD, RAX, true>(s, bcol, vals, invd, b, x, reset, done, st, ru);
+    else
+        launch_bsr_d<LG, BS, UP, PAD, RAX, false>(s, bcol, vals, invd, b, x, reset, done, st, ru);
 }
 
 // pad: output / re-arm vectors (and the upper sweep's right-hand side)

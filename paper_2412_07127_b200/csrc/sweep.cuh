@@ -13,14 +13,19 @@
 #ifndef BSR_MINB
 #define BSR_MINB 2
 #endif
-// node-blocked sweep CTA: 128 threads, 6 resident per SM (24 warps at <= 80
-// registers per thread; a few bytes of spill). Measured on configs[2]
-// (per sweep): 5/SM 0.934 ms, 6/SM 0.904, 7/SM 1.02, 8/SM 1.09 (spills)
+// node-blocked sweep CTA: 128 threads, 7 resident per SM (28 warps at <= 72
+// registers; a few bytes of spill), entries prefetched into L1 one item
+// ahead (slot records two ahead). Measured on configs[2], production build
+// (no developer probes), per sweep: 6/SM 0.868 ms, 7/SM 0.859, 7/SM with
+// one-item prefetch 0.849, 8/SM 1.02 (spills)
 #ifndef BSR_THREADS
 #define BSR_THREADS 128
 #endif
 #ifndef BSR_CTAS
-#define BSR_CTAS 6
+#define BSR_CTAS 7
+#endif
+#ifndef BSR_PF
+#define BSR_PF 1
 #endif
 
 
@@ -631,7 +636,9 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
     BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
     BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+#if BSR_PF >= 2
     BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+#endif
     double rhs0[BS], rhs1[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) {
@@ -652,9 +659,15 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         }
     };
     prefetch(m);
+#if BSR_PF >= 2
     prefetch(m1);
+#endif
     while (it < nitems) {
+#if BSR_PF >= 2
         prefetch(m2);
+#else
+        prefetch(m1);
+#endif
         long long tr0 = 0;
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         bsr_item<LG, BS, UPPER, PAD, RAX>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0,
@@ -662,8 +675,12 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         it += nwarps;
         m = m1;
         m1 = m2;
+#if BSR_PF >= 2
         m2 = m3;
         m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+#else
+        m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+#endif
 #pragma unroll
         for (int t = 0; t < BS; ++t) {
             rhs0[t] = rhs1[t];
@@ -672,7 +689,9 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     }
 }
 
-template <int LG, int BS, bool UPPER, bool PAD, bool RAX = false>
+// DEV: developer probes (tune word, per-item trace) compiled in; the
+// production instantiation drops their branches and registers.
+template <int LG, int BS, bool UPPER, bool PAD, bool RAX = false, bool DEV = false>
 __global__ void __launch_bounds__(BSR_THREADS, BSR_CTAS)
 bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals,
@@ -681,7 +700,8 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
     if (done && *done) return;
     bsr_sweep<LG, BS, UPPER, PAD, RAX>(nitems, srec, bcol, vals, invd, rhs, out, reset,
                                        (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
-                                       (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, tune, trace, ru);
+                                       (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, DEV ? tune : 0,
+                                       DEV ? trace : nullptr, ru);
 }
 
 // ------------------------------------------------------------------------
