@@ -449,10 +449,14 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
     const int gl = lane % LG;
     const bool active = m.blk >= 0;
     const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
-    int64_t mrp[BS + 1];
-    slot_rows<BS>(m, mrp);
+    // 32-bit entry offsets (slot records guarantee < 2^32): one wide
+    // multiply-add per address instead of 64-bit add pairs
+    uint32_t mrp[BS + 1];
+    mrp[0] = m.r0;
+#pragma unroll
+    for (int t = 0; t < BS; ++t) mrp[t + 1] = mrp[t] + ((m.lens >> (10 * t)) & 1023u);
     // off-block entries of row t start at ob[t]; nb neighbour blocks
-    int64_t ob[BS];
+    uint32_t ob[BS];
 #pragma unroll
     for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
     const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
