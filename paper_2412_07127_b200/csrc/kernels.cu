@@ -60,6 +60,66 @@ spmv_bsr_kernel(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
     }
 }
 
+// y = A x for node-blocked A with 32-bit entry / block-column offsets
+// (nnz < 2^32): the row records fit five registers, so five 256-thread CTAs
+// per SM stay resident without spills (40 warps of loads in flight).
+template <int BS>
+__global__ void __launch_bounds__(256, 5)
+spmv_bsr32_kernel(int nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
+                  const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ x,
+                  double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    struct Row32 {
+        uint32_t r[BS];
+        uint32_t c0;
+        int cnt;
+    };
+    auto row32 = [&](int b) {
+        Row32 o{};
+        if (b < nb) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) o.r[t] = static_cast<uint32_t>(__ldg(rp + static_cast<int64_t>(b) * BS + t));
+            const int64_t c0 = __ldg(bp + b);
+            o.c0 = static_cast<uint32_t>(c0);
+            o.cnt = static_cast<int>(__ldg(bp + b + 1) - c0);
+        }
+        return o;
+    };
+    Row32 m = row32(gw);
+    for (int b = gw; b < nb; b += nw) {
+        const Row32 mn = row32(b + nw);
+        double acc[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+        for (int n = lane; n < m.cnt; n += 32) {
+            const int32_t xc = __ldg(bcol + (m.c0 + n));
+            double a[BS][BS], xv[BS];
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) a[t][c] = __ldg(vals + (m.r[t] + BS * n + c));
+#pragma unroll
+            for (int c = 0; c < BS; ++c) xv[c] = __ldg(x + xc + c);
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<32>(acc[t]);
+        if (lane < BS) {
+            double v = acc[0];
+#pragma unroll
+            for (int t = 1; t < BS; ++t)
+                if (lane == t) v = acc[t];
+            y[static_cast<int64_t>(b) * BS + lane] = v;
+        }
+        m = mn;
+    }
+}
+
 __global__ void gather_kernel(int64_t m, const int64_t* __restrict__ idx, const double* __restrict__ src,
                               double* __restrict__ dst) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -110,7 +170,11 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
     if (a.an && a.an->a_bsr) {  // node-blocked: one column index per block
         const BlockCols& bc = a.an->abc;
         static const unsigned g3 = resident_ctas(spmv_bsr_kernel<3>), g2 = resident_ctas(spmv_bsr_kernel<2>);
-        if (a.an->bs == 3)
+        static const unsigned g32 = resident_ctas(spmv_bsr32_kernel<3>);
+        if (a.an->bs == 3 && a.a.nnz < (1LL << 32) && bc.bcol.n < (1LL << 32) && n / 3 < (1LL << 31))
+            spmv_bsr32_kernel<3><<<g32, 256, 0, st>>>(static_cast<int>(n / 3), a.a.rp.p, bc.bp.p, bc.bcol.p,
+                                                       a.a.vals.p, x, y);
+        else if (a.an->bs == 3)
             spmv_bsr_kernel<3><<<g3, 256, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);
         else
             spmv_bsr_kernel<2><<<g2, 256, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, x, y);

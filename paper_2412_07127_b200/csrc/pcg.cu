@@ -156,8 +156,10 @@ k_pupdate4(int64_t n, const double* __restrict__ z, double* __restrict__ p4, con
 
 // q = A p (padded p) and pAp: k_spmv_bsr_pap<3> with one 256-bit gather
 // per neighbour block; same per-row summation order.
+// 5 CTAs/SM (40 warps at 48 registers): configs[2] product 0.652 ms at 4,
+// 0.644 at 5, 0.813 at 6
 #ifndef PAP4_MINB
-#define PAP4_MINB 4
+#define PAP4_MINB 5
 #endif
 __global__ void __launch_bounds__(kT, PAP4_MINB)
 k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
@@ -169,22 +171,40 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
     }
     constexpr int BS = 3;
     const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * kT) >> 5;
+    const int gw = static_cast<int>((blockIdx.x * kT + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * kT) >> 5);
     double loc = 0.0;
-    BsrRow<BS> m = bsr_row<BS>(gw, nb, rp, bp);
-    for (int64_t b = gw; b < nb; b += nw) {
-        const BsrRow<BS> mn = bsr_row<BS>(b + nw, nb, rp, bp);
+    // 32-bit row / block-column offsets (nnz(A) < 2^32, checked by the
+    // launcher): five registers per row record instead of nine
+    struct Row32 {
+        uint32_t r[BS];
+        uint32_t c0;
+        int cnt;
+    };
+    auto row32 = [&](int b) {
+        Row32 o{};
+        if (b < nb) {
+#pragma unroll
+            for (int t = 0; t < BS; ++t) o.r[t] = static_cast<uint32_t>(__ldg(rp + static_cast<int64_t>(b) * BS + t));
+            const int64_t c0 = __ldg(bp + b);
+            o.c0 = static_cast<uint32_t>(c0);
+            o.cnt = static_cast<int>(__ldg(bp + b + 1) - c0);
+        }
+        return o;
+    };
+    Row32 m = row32(gw);
+    for (int b = gw; b < nb; b += nw) {
+        const Row32 mn = row32(b + nw);
         double acc[BS] = {0.0, 0.0, 0.0};
         for (int n = lane; n < m.cnt; n += 32) {
-            const int32_t xc = __ldg(bcol + m.c0 + n);
+            const int32_t xc = __ldg(bcol + (m.c0 + n));
             double a[BS][BS];
 #pragma unroll
             for (int t = 0; t < BS; ++t)
 #pragma unroll
-                for (int c = 0; c < BS; ++c) a[t][c] = __ldg(vals + m.r[t] + BS * n + c);
+                for (int c = 0; c < BS; ++c) a[t][c] = __ldg(vals + (m.r[t] + BS * n + c));
             double xv[4];
-            ldg256(p4 + 4 * static_cast<int64_t>(xc / 3), xv[0], xv[1], xv[2], xv[3]);
+            ldg256(p4 + 4 * static_cast<uint32_t>(xc / 3), xv[0], xv[1], xv[2], xv[3]);
 #pragma unroll
             for (int t = 0; t < BS; ++t)
 #pragma unroll
@@ -195,9 +215,9 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
         if (lane == 0) {
 #pragma unroll
             for (int t = 0; t < BS; ++t) {
-                const int64_t row = b * BS + t;
+                const int64_t row = static_cast<int64_t>(b) * BS + t;
                 q[row] = acc[t];
-                loc = fma(p4[4 * b + t], acc[t], loc);
+                loc = fma(p4[4 * static_cast<int64_t>(b) + t], acc[t], loc);
             }
         }
         m = mn;
@@ -644,7 +664,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     const bool fused = an && an->fused_up;
     // padded p for the node-blocked 3x3 product (PCLAB_PADP=0: plain p)
     static const bool padp_env = !(getenv("PCLAB_PADP") && atoi(getenv("PCLAB_PADP")) == 0);
-    const bool padp = padp_env && an && an->a_bsr && an->bs == 3 && !fused;
+    // (k_spmv_bsr_pap4 indexes A's entries and block columns with 32 bits)
+    const bool padp = padp_env && an && an->a_bsr && an->bs == 3 && !fused && a.a.nnz < (1LL << 32) &&
+                      an->abc.bcol.n < (1LL << 32);
     pa.alloc(padp ? 4 * (n / 3) : n);
     // sweep vectors y, z padded too (node-blocked 3x3 sweeps): 256-bit polls
     // and publications (bsr_item PAD); PCLAB_PADZ=0 keeps them plain
