@@ -276,6 +276,7 @@ static void launch_bsr_d(const Schedule& s, const int32_t* bcol, const double* v
                                                          BSR_THREADS, 0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
+    if (s.nitems * s.per_item >= (1LL << 31)) throw DimensionError("node-blocked sweep: too many schedule slots");
     const unsigned grid = std::min(trsv_grid(s, 5.0, BSR_THREADS / 32), cap);  // ~all resident warps
     bsr_trsv_kernel<LG, BS, UP, PAD, RAX, DEV><<<grid, BSR_THREADS, 0, st>>>(
         s.nitems, s.slot_rp.p, bcol, vals, invd, b, x, reset, done, trsv_tune(), g_trace, ru);

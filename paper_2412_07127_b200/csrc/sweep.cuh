@@ -371,6 +371,11 @@ __device__ __forceinline__ BsrSlot bsr_slot(int64_t it, int64_t nitems, int G, i
     return BsrSlot{v.x, static_cast<uint32_t>(v.y), static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
 }
 
+__device__ __forceinline__ BsrSlot bsr_slot32(int it, int nitems, int G, int grp, const int32_t* __restrict__ srec) {
+    const int4 v = it < nitems ? __ldg(reinterpret_cast<const int4*>(srec) + (it * G + grp)) : make_int4(-1, 0, 0, 0);
+    return BsrSlot{v.x, static_cast<uint32_t>(v.y), static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+}
+
 template <int BS>
 __device__ __forceinline__ void slot_rows(const BsrSlot& m, int64_t (&rp)[BS + 1]) {
     rp[0] = m.r0;
@@ -636,12 +641,14 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     auto rhs_at = [&](int64_t i) { return RAX ? fma(-alpha, ru.q[i], rhs[i]) : rhs[i]; };
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
-    int64_t it = warp;
-    BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
-    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
-    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+    // 32-bit item indices (items * G < 2^31, checked by the launcher)
+    const int nit = static_cast<int>(nitems), nw = static_cast<int>(nwarps);
+    int it = static_cast<int>(warp);
+    BsrSlot m = bsr_slot32(it, nit, G, grp, srec);
+    BsrSlot m1 = bsr_slot32(it + nw, nit, G, grp, srec);
+    BsrSlot m2 = bsr_slot32(it + 2 * nw, nit, G, grp, srec);
 #if BSR_PF >= 2
-    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+    BsrSlot m3 = bsr_slot32(it + 3 * nw, nit, G, grp, srec);
 #endif
     double rhs0[BS], rhs1[BS];
 #pragma unroll
@@ -666,7 +673,7 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
 #if BSR_PF >= 2
     prefetch(m1);
 #endif
-    while (it < nitems) {
+    while (it < nit) {
 #if BSR_PF >= 2
         prefetch(m2);
 #else
@@ -676,14 +683,14 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         bsr_item<LG, BS, UPPER, PAD, RAX>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0,
                                           ru.rnew);
-        it += nwarps;
+        it += nw;
         m = m1;
         m1 = m2;
 #if BSR_PF >= 2
         m2 = m3;
-        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
+        m3 = bsr_slot32(it + 3 * nw, nit, G, grp, srec);
 #else
-        m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
+        m2 = bsr_slot32(it + 2 * nw, nit, G, grp, srec);
 #endif
 #pragma unroll
         for (int t = 0; t < BS; ++t) {

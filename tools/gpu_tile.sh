@@ -1,3 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/tall5.log 2>&1; echo RC $? >> gpurun_out/tall5.log
-timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b8.log 2>&1
-timeout 600 python bench.py --bw-elasticity > gpurun_out/bwe2.log 2>&1
+for i in 1 2; do timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/i32.log 2>&1; done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_variants.py -x -q > gpurun_out/ti32.log 2>&1
