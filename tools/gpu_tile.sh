@@ -1,2 +1,3 @@
-for i in 1 2; do timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/i32.log 2>&1; done
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_variants.py -x -q > gpurun_out/ti32.log 2>&1
+for env in "PCLAB_X=1" "PCLAB_LIB=build/var/lib_7_0.so" "PCLAB_LIB=build/var/lib_8_0.so PCLAB_TRSV_DEPTH=6"; do
+  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/ra.log 2>&1
+done
