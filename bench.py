@@ -450,7 +450,7 @@ def run_bw_elasticity(args):
             "metric": "kernel_bandwidth", "workload": w.name, "n": n, "nnz": nnz, "factor": factor,
             "levels": [info["block_levels_lower"], info["block_levels_upper"]], "peak_gbs": hbm,
             "peak_source": peak_kind, "l2": "flushed before every launch",
-            "note": "stand-alone kernels on plain vectors (the PCG loop runs the padded-vector variants)",
+            "note": "stand-alone API calls (pclab_spmv_device / pclab_trsv_device; 3x3 sweeps run on padded copies, copies included)",
             "kernels": kern}), flush=True)
         del pc, a
 

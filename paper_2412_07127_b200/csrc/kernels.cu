@@ -120,6 +120,15 @@ spmv_bsr32_kernel(int nb, const int64_t* __restrict__ rp, const int64_t* __restr
     }
 }
 
+// plain <-> padded (4 doubles per 3-dof node) vector copies
+__global__ void pad_copy_kernel(int64_t n, const double* __restrict__ src, double* __restrict__ dst, bool to_pad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int64_t k = 4 * (i / 3) + i % 3;
+    if (to_pad) dst[k] = src[i];
+    else dst[i] = src[k];
+}
+
 __global__ void gather_kernel(int64_t m, const int64_t* __restrict__ idx, const double* __restrict__ src,
                               double* __restrict__ dst) {
     const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -480,6 +489,27 @@ void trsv(const Analysis& an, const double* vals, const double* invd, bool upper
     if (tf) {
         tb.alloc(4 * (s.nitems * s.per_item + s.nblocks));
         g_trace = tb.p;
+    }
+    // 3x3 node-blocked sweeps run on the padded layout of the PCG loop
+    // (4 doubles per node: 256-bit polls / publications): the right-hand
+    // side of the backward sweep and the output go through padded copies
+    static const bool padz_env = !(getenv("PCLAB_PADZ") && atoi(getenv("PCLAB_PADZ")) == 0);
+    const bool pad = padz_env && an.bsr && an.bs == 3 && !tf && s.tile.ntiles == 0;
+    if (pad) {
+        const int64_t n = an.lower.n, n4 = 4 * (n / 3);
+        DevBuf<double> x4(n4), b4;
+        fill_pending(x4.p, n4, st);
+        if (upper) {
+            b4.alloc(n4);
+            CK(cudaMemsetAsync(b4.p, 0, b4.bytes(), st));
+            pad_copy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, b, b4.p, true);
+            CK_LAUNCH();
+        }
+        launch_trsv(an, vals, invd, upper, upper ? b4.p : b, x4.p, nullptr, nullptr, ctr.p, st, true);
+        pad_copy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, x4.p, x, false);
+        CK_LAUNCH();
+        CK(cudaStreamSynchronize(st));
+        return;
     }
     launch_trsv(an, vals, invd, upper, b, x, nullptr, nullptr, ctr.p, st);
     CK(cudaStreamSynchronize(st));

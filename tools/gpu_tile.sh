@@ -1,3 +1,2 @@
-for env in "PCLAB_X=1" "PCLAB_LIB=build/var/lib_7_0.so" "PCLAB_LIB=build/var/lib_8_0.so PCLAB_TRSV_DEPTH=6"; do
-  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/ra.log 2>&1
-done
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_variants.py tests/test_gpu_fullsize.py -x -q > gpurun_out/tpad.log 2>&1; echo RC $? >> gpurun_out/tpad.log
+timeout 300 python tools/trsv_time.py elasticity_q1_118 > gpurun_out/tpadt.log 2>&1
