@@ -341,13 +341,25 @@ static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uv
         an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
 }
 
+#ifndef RR_DEPTH
+#define RR_DEPTH 6.0
+#endif
 template <int LG, int BS, bool UP, int CH>
 static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd, const double* b,
                         double* x, double* reset, const int* done, cudaStream_t st) {
-    static const unsigned cap = resident_ctas(rr_trsv_kernel<LG, BS, UP, CH>);
-    const unsigned grid = std::min(trsv_grid(s, 3.0), cap);
-    rr_trsv_kernel<LG, BS, UP, CH><<<grid, 256, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals, invd, b,
-                                                          x, reset, done, trsv_tune());
+    static unsigned cap = 0;
+    if (!cap) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rr_trsv_kernel<LG, BS, UP, CH>, RR_THREADS, 0));
+        cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+    }
+    const unsigned grid = std::min(trsv_grid(s, RR_DEPTH, RR_THREADS / 32), cap);
+    if (trsv_tune() != 0)
+        rr_trsv_kernel<LG, BS, UP, CH, true><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals,
+                                                                          invd, b, x, reset, done, trsv_tune());
+    else
+        rr_trsv_kernel<LG, BS, UP, CH, false><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals,
+                                                                           invd, b, x, reset, done, 0);
 }
 
 // Tiled sweep: one 512-thread CTA per tile, all resident (1 per SM).

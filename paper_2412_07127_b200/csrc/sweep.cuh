@@ -963,15 +963,24 @@ tile_trsv_kernel(const int64_t* __restrict__ tbeg, const int32_t* __restrict__ t
 // one item ahead, dependency values polled directly -- with lanes over the
 // block's off-block entries (lane gl takes entries gl, gl + LG, ... of the
 // block's rows in order) instead of over neighbour blocks.
-template <int LG, int BS, bool UPPER, int CH>
-__global__ void __launch_bounds__(256, BSR_MINB)
+// RR_THREADS-thread CTAs, RR_CTAS resident per SM; DEV: the poll back-off
+// knob compiled in (the production build drops it)
+// (diffusion 256^3, per sweep: 256 x 4/SM 1.18 ms, 128 x 9/SM 1.15, 128 x 12/SM 1.28)
+#ifndef RR_THREADS
+#define RR_THREADS 128
+#endif
+#ifndef RR_CTAS
+#define RR_CTAS 9
+#endif
+template <int LG, int BS, bool UPPER, int CH, bool DEV = false>
+__global__ void __launch_bounds__(RR_THREADS, RR_CTAS)
 rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                const int32_t* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ invd,
                const double* rhs, double* out, double* reset, const int* __restrict__ done, int tune) {
     if (done && *done) return;
     constexpr int G = 32 / LG;
     constexpr int NIB = BS * (BS - 1) / 2;
-    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+    const unsigned sleep_ns = DEV ? static_cast<unsigned>(tune >> 8) : 0u;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;

@@ -1,2 +1,2 @@
-python bench.py > gpurun_out/bench2.log 2> gpurun_out/bench2.err
-python bench.py --bw-elasticity > gpurun_out/bw_el2.log 2> gpurun_out/bw_el2.err
+timeout 300 python tools/trsv_time.py diffusion_fv_256 >> gpurun_out/rr2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/trr.log 2>&1; echo RC $? >> gpurun_out/trr.log
