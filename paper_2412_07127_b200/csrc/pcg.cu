@@ -631,7 +631,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     h.rel_tol = rel_tol;
     h.max_iters = max_iters;
     CK(cudaMemcpyAsync(S.p, &h, sizeof h, cudaMemcpyHostToDevice, st));
-    const unsigned vgrid = static_cast<unsigned>(sm_count() * 4);
+    // vector kernels: 8 CTAs per SM (axpy 58 -> 45 us, dot 26 -> 25 us on configs[2])
+    static const int vmul = std::min(getenv("PCLAB_VGRID") ? atoi(getenv("PCLAB_VGRID")) : 8, 8);
+    const unsigned vgrid = static_cast<unsigned>(sm_count() * vmul);
     const unsigned sgrid = static_cast<unsigned>(sm_count() * 8);
     if (n) k_dot<<<vgrid, kT, 0, st>>>(n, b, b, S.p, part.p, 2);
     CK_LAUNCH();

@@ -1,2 +1,3 @@
-timeout 300 python tools/trsv_time.py diffusion_fv_256 >> gpurun_out/rr2.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/trr.log 2>&1; echo RC $? >> gpurun_out/trr.log
+for env in "PCLAB_VGRID=4" "PCLAB_VGRID=8" "PCLAB_VGRID=2"; do
+  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/vg.log 2>&1
+done
