@@ -299,11 +299,8 @@ ic0_mask_kernel(int64_t nitems, int per_item, int bs, const int32_t* __restrict_
 // order (ascending shared column, explicitly rounded), so bit-identical;
 // ~BS x fewer instructions per row than ic0_mask_kernel and no polling
 // between the rows of a block.
-#ifndef IC0B_MINB
-#define IC0B_MINB 1
-#endif
 template <int BS, int C>
-__global__ void __launch_bounds__(256, IC0B_MINB)
+__global__ void __launch_bounds__(256)
 ic0_block_kernel(int64_t nslots, const int32_t* __restrict__ slots, const int64_t* __restrict__ lrp,
                  const int32_t* __restrict__ lcols, const double* __restrict__ avals,
                  const unsigned long long* __restrict__ mu, const unsigned long long* __restrict__ mj, double shift,
