@@ -1,3 +1,4 @@
-for env in "PCLAB_VGRID=4" "PCLAB_VGRID=8" "PCLAB_VGRID=2"; do
-  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/vg.log 2>&1
-done
+python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err
+python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/b1.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+      --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
