@@ -197,6 +197,74 @@ ic0_masks(int64_t nunits, int bs, const int64_t* __restrict__ lrp, const int32_t
     }
 }
 
+// The same masks from the block-column view (node-blocked L, bs = 3):
+// row 3I+r's off-block entry p = 3k + c is column 3K + c, K = N_I[k]. Its
+// row (3K + c) holds the off-block blocks N_K and in-block columns 3K..3K+c-1,
+// so the matches are every component of each K' in N_I[0..k) that is also
+// in N_K (row j position 3m' + c', m' = index of K' in N_K), plus columns
+// 3K + c' < 3K + c (row j position 3|N_K| + c'). One lane per neighbour
+// block merges two lists of <= 32 blocks instead of two rows of scalars.
+__global__ void __launch_bounds__(256)
+ic0_masks_bsr(int64_t nbk, const int64_t* __restrict__ lrp, const int64_t* __restrict__ bp,
+              const int32_t* __restrict__ bcol, unsigned long long* __restrict__ mu,
+              unsigned long long* __restrict__ mj) {
+    constexpr int BS = 3;
+    __shared__ int32_t nbr[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t I = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (I >= nbk) return;
+    const int64_t b0 = bp[I];
+    const int ni = static_cast<int>(bp[I + 1] - b0);  // <= 21 (checked by the caller: 3 ni + 2 < 64)
+    if (lane < ni) nbr[w][lane] = bcol[b0 + lane] / BS;
+    __syncwarp();
+    int64_t beg[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) beg[r] = lrp[I * BS + r];
+    if (lane < ni) {
+        const int k = lane;
+        const int32_t K = nbr[w][k];
+        const int64_t c0 = bp[K];
+        const int nk = static_cast<int>(bp[K + 1] - c0);
+        unsigned long long bu = 0, bj = 0;
+        int u = 0, q = 0;
+        int32_t cq = q < nk ? bcol[c0] / BS : INT_MAX;
+        while (u < k && q < nk) {
+            const int32_t cu = nbr[w][u];
+            if (cu < cq) {
+                ++u;
+            } else if (cq < cu) {
+                ++q;
+                cq = q < nk ? bcol[c0 + q] / BS : INT_MAX;
+            } else {
+                bu |= 7ULL << (BS * u);
+                bj |= 7ULL << (BS * q);
+                ++u;
+                ++q;
+                cq = q < nk ? bcol[c0 + q] / BS : INT_MAX;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            // components c' < c of block K itself
+            const unsigned long long own_u = ((1ULL << c) - 1) << (BS * k);
+            const unsigned long long own_j = ((1ULL << c) - 1) << (BS * nk);
+#pragma unroll
+            for (int r = 0; r < BS; ++r) {
+                mu[beg[r] + BS * k + c] = bu | own_u;
+                mj[beg[r] + BS * k + c] = bj | own_j;
+            }
+        }
+    }
+    // in-block entries of rows r >= 1 (position p = 3 ni + s, column 3I + s)
+    for (int r = 1; r < BS; ++r)
+        for (int sidx = lane; sidx < r; sidx += 32) {
+            const int p = BS * ni + sidx;
+            const unsigned long long m = (1ULL << p) - 1;
+            mu[beg[r] + p] = m;
+            mj[beg[r] + p] = m;
+        }
+}
+
 // Numeric half: the ic0_kernel schedule (warp per row, rows in (level,
 // index) order, lane t owns entry t, step u finalises entry u and
 // broadcasts l_{i c_u}), but a lane learns from its masks whether step u
@@ -486,10 +554,19 @@ int ic0_factor(const Matrix& a, const Analysis& an, double* out, cudaStream_t st
             mj.alloc(L.nnz);
         }
         mask_id = an.id;
-        const int mbs = an.bsr ? an.bs : 1;
-        const int64_t units = n / mbs;
-        ic0_masks<<<static_cast<unsigned>((units * 32 + 255) / 256), 256, 0, st>>>(units, mbs, L.rp.p, L.cols.p,
-                                                                                   mu.p, mj.p);
+        static const bool bsr_masks = !(getenv("PCLAB_IC0_BSR_MASKS") && atoi(getenv("PCLAB_IC0_BSR_MASKS")) == 0);
+        if (bsr_masks && an.bsr && an.bs == 3 && maxlen <= 64) {
+            // (maxlen <= 64 bounds 3 |N| + 2 for every block row, so all
+            // bit positions fit)
+            const int64_t nbk = n / 3;
+            ic0_masks_bsr<<<static_cast<unsigned>((nbk * 32 + 255) / 256), 256, 0, st>>>(nbk, L.rp.p, an.lbc.bp.p,
+                                                                                          an.lbc.bcol.p, mu.p, mj.p);
+        } else {
+            const int mbs = an.bsr ? an.bs : 1;
+            const int64_t units = n / mbs;
+            ic0_masks<<<static_cast<unsigned>((units * 32 + 255) / 256), 256, 0, st>>>(units, mbs, L.rp.p, L.cols.p,
+                                                                                       mu.p, mj.p);
+        }
         CK_LAUNCH();
     }
     for (int attempt = 0;; ++attempt) {
