@@ -1,4 +1,6 @@
-timeout 600 python -m pytest tests/test_gpu_variants.py -x -q -k ic0 > gpurun_out/tm.log 2>&1; echo RC $? >> gpurun_out/tm.log
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "ic0 or config" > gpurun_out/tm2.log 2>&1; echo RC $? >> gpurun_out/tm2.log
-timeout 300 python tools/gnn_time.py elasticity_q1_118 > gpurun_out/gm.log 2>&1
-timeout 300 python bench.py --steps 2 --warmup 2 --no-cpu-baseline > gpurun_out/bm.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/tfinal.log 2>&1; echo RC $? >> gpurun_out/tfinal.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo RC $? >> gpurun_out/smoke.log
+python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err
+python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/b1.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+      --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
