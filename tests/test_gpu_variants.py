@@ -49,7 +49,8 @@ print("ok", rep["iterations"], ro["iterations"])
 @pytest.mark.parametrize("env", [{"PCLAB_FUSE": "1"}, {"PCLAB_CHAIN": "1"}, {"PCLAB_BSR": "0"},
                                  {"PCLAB_CHAIN": "1", "PCLAB_CHAIN_K": "3"}, {"PCLAB_TILE": "0"},
                                  {"PCLAB_TILES": "3", "PCLAB_TILE_K": "4"}, {"PCLAB_TILE_RING": "64"},
-                                 {"PCLAB_RAX": "1"}, {"PCLAB_PADZ": "0"}, {"PCLAB_PADP": "0"}])
+                                 {"PCLAB_RAX": "1"}, {"PCLAB_PADZ": "0"}, {"PCLAB_PADP": "0"},
+                                 {"PCLAB_LEVEL_QUEUE": "0"}])
 def test_variant_parity(env):
     e = dict(os.environ, **env)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=e, cwd=ROOT,
@@ -108,14 +109,15 @@ print(h.hexdigest())
 
 
 def test_ic0_mask_kernel_bit_identical_to_merge_walk():
-    """The mask-driven IC(0) (symbolic masks + mask kernel, per node block on
-    elasticity, per row on Poisson / diffusion) and the merge-walk kernel
-    (PCLAB_IC0_MASKS=0) produce the same factor bits."""
+    """The mask-driven IC(0) (symbolic masks from the block-column view or
+    from scalar rows (PCLAB_IC0_BSR_MASKS=0) + the block / row mask kernels)
+    and the merge-walk kernel (PCLAB_IC0_MASKS=0) produce the same factor
+    bits."""
     outs = []
-    for env in ({"PCLAB_IC0_MASKS": "0"}, {}):
+    for env in ({"PCLAB_IC0_MASKS": "0"}, {}, {"PCLAB_IC0_BSR_MASKS": "0"}):
         e = dict(os.environ, **env)
         out = subprocess.run([sys.executable, "-c", IC0.format(root=ROOT)], env=e, cwd=ROOT,
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stdout + out.stderr
         outs.append(out.stdout.strip())
-    assert outs[0] == outs[1], outs
+    assert len(set(outs)) == 1, outs
