@@ -664,13 +664,17 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         rhs1[t] = m1.blk >= 0 ? rhs_at(static_cast<int64_t>(m1.blk) * RS + t) : 0.0;
     }
 #endif
+    // one 128-byte line per lane covers a block's rows up to 16 * LG
+    // doubles (3 elasticity rows: ~125); longer rows take the loop
     auto prefetch = [&](const BsrSlot& q) {
         if (q.blk >= 0) {
-            int64_t rq[BS + 1];
-            slot_rows<BS>(q, rq);
-            const int64_t e0 = rq[0], e1 = rq[BS];
-            for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
+            const uint32_t e0 = q.r0 & ~15u;
+            uint32_t e1 = q.r0;
+#pragma unroll
+            for (int t = 0; t < BS; ++t) e1 += (q.lens >> (10 * t)) & 1023u;
+            uint32_t a = e0 + 16u * gl;
+            if (a < e1) asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
+            for (a += 16u * LG; a < e1; a += 16u * LG) asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
             if (gl == 0) {
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(bcol + q.bp));
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + static_cast<int64_t>(q.blk) * BS));

@@ -1,1 +1,1 @@
-timeout 1200 python -m pytest tests/test_gpu_variants.py -q > gpurun_out/tv2.log 2>&1; echo RC $? >> gpurun_out/tv2.log
+for i in 1 2; do timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/pfl.log 2>&1; done
