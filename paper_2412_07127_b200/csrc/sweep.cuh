@@ -681,14 +681,16 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             }
         }
     };
+#if BSR_PF >= 1
     prefetch(m);
+#endif
 #if BSR_PF >= 2
     prefetch(m1);
 #endif
     while (it < nit) {
 #if BSR_PF >= 2
         prefetch(m2);
-#else
+#elif BSR_PF == 1
         prefetch(m1);
 #endif
         long long tr0 = 0;

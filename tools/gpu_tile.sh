@@ -1,4 +1,3 @@
-python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err
-python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/rk.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"bsr_trsv_kernel|k_spmv_bsr_pap4" -s 2 -c 3 \
-      -o gpurun_out/loop python tools/run_kernels.py elasticity_q1_118 0 1 > gpurun_out/ncu_loop.log 2>&1
+for env in "PCLAB_LIB=build/var/lib_7_0.so" "PCLAB_LIB=build/var/lib_8_0.so PCLAB_TRSV_DEPTH=6" "PCLAB_LIB=build/var/lib_8_1.so PCLAB_TRSV_DEPTH=6"; do
+  env $env timeout 300 python tools/trsv_time.py elasticity_q1_118 >> gpurun_out/pf0.log 2>&1
+done
