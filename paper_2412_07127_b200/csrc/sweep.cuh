@@ -699,8 +699,18 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
         // loaded as the item starts: only the diagonal solve (after the
         // dependency polls) consumes it
         double rhs0[BS];
+        if constexpr (RS == 4 && !RAX) {  // padded y: one 256-bit load
+            double d3 = 0.0;
+            rhs0[0] = rhs0[1] = rhs0[2] = 0.0;
+            if (m.blk >= 0)
+                asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                             : "=d"(rhs0[0]), "=d"(rhs0[1]), "=d"(rhs0[2]), "=d"(d3)
+                             : "l"(rhs + 4 * static_cast<int64_t>(m.blk)));
+            (void)d3;
+        } else {
 #pragma unroll
-        for (int t = 0; t < BS; ++t) rhs0[t] = m.blk >= 0 ? rhs_at(static_cast<int64_t>(m.blk) * RS + t) : 0.0;
+            for (int t = 0; t < BS; ++t) rhs0[t] = m.blk >= 0 ? rhs_at(static_cast<int64_t>(m.blk) * RS + t) : 0.0;
+        }
 #endif
         bsr_item<LG, BS, UPPER, PAD, RAX>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0,
                                           ru.rnew);
