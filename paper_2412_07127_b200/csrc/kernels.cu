@@ -36,6 +36,26 @@ spmv_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict
     }
 }
 
+// short scalar rows: a warp per 32 consecutive rows (tile_rows_dot), the
+// next tile's row pointers loaded a tile ahead
+__global__ void TILE_LB(256)
+spmv_tile_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                 const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y) {
+    __shared__ double sh[8][kTileCh];
+    const int lane = threadIdx.x & 31;
+    const int64_t nt = (n + 31) / 32;
+    const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    RowSpan s = row_span(rp, n, gw * 32 + lane);
+    for (int64_t t = gw; t < nt; t += nw) {
+        const RowSpan sn = row_span(rp, n, (t + nw) * 32 + lane);
+        const double acc = tile_rows_dot(s, cols, vals, x, sh[threadIdx.x >> 5], lane);
+        const int64_t row = t * 32 + lane;
+        if (row < n) y[row] = acc;
+        s = sn;
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(256)
 spmv_bsr_kernel(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
@@ -166,7 +186,8 @@ int spmv_lanes(const Matrix& a) {
     // Few lanes per row, many rows per warp: on the 81-entry elasticity rows
     // 4 lanes x 8 loads in flight beat 8/16/32 lanes (measured, configs[2]:
     // 1.04 vs 1.09/1.25/1.18 ms). Code 5 = 4 lanes with 8 loads per round.
-    int l = avg > 48 ? 5 : 4;
+    // Code 1 = a warp per 32 short rows (tile_rows_dot; 7-point stencils).
+    int l = avg > 48 ? 5 : (avg <= 12 ? 1 : 4);
     if (avg > 200) l = 32;
     if (getenv("PCLAB_SPMV_LPR")) l = atoi(getenv("PCLAB_SPMV_LPR"));
     return l;
@@ -191,6 +212,11 @@ void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st) {
         return;
     }
     switch (spmv_lanes(a)) {
+        case 1: {
+            static const unsigned gt = resident_ctas(spmv_tile_kernel);
+            spmv_tile_kernel<<<gt, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y);
+            break;
+        }
         case 4:
         case 5: spmv_kernel<4><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;
         case 8: spmv_kernel<8><<<grid, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, x, y); break;

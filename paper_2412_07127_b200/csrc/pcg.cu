@@ -129,6 +129,46 @@ k_spmv_pap(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict_
     }
 }
 
+// q = A p and pAp for short scalar rows: a warp per 32 consecutive rows
+// (tile_rows_dot), row pointers a tile ahead.
+__global__ void TILE_LB(kT)
+k_spmv_tile_pap(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                const double* __restrict__ vals, const double* __restrict__ p, double* __restrict__ q,
+                Scal* S, double* part) {
+    if (S->done) return;
+    __shared__ double sh[kT / 32][kTileCh];
+    const int lane = threadIdx.x & 31;
+    const int64_t nt = (n + 31) / 32;
+    const int64_t gw = (blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * kT) >> 5;
+    double loc = 0.0;
+    RowSpan s = row_span(rp, n, gw * 32 + lane);
+    for (int64_t t = gw; t < nt; t += nw) {
+        const RowSpan sn = row_span(rp, n, (t + nw) * 32 + lane);
+        const double acc = tile_rows_dot(s, cols, vals, p, sh[threadIdx.x >> 5], lane);
+        const int64_t row = t * 32 + lane;
+        if (row < n) {
+            q[row] = acc;
+            loc = fma(p[row], acc, loc);
+        }
+        s = sn;
+    }
+    double tot;
+    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
+        S->pap = tot;
+        if (!(tot > 0.0)) {
+            S->error = 1;
+            S->done = 1;
+        } else {
+            S->alpha = S->rz / tot;
+        }
+        S->ctr[0] = 0;
+        S->ctr[1] = 0;
+        S->ctr[2] = 0;
+        S->ctr[3] = 0;
+    }
+}
+
 // ---- padded p (node-blocked A, bs = 3): p stored as 4 doubles per node
 // (32-byte aligned, pad = 0), so the product gathers a neighbour's three
 // values with ONE 256-bit load instead of three 8-byte loads (a third of
@@ -711,6 +751,11 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK_LAUNCH();
     // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
+    static const unsigned tgrid = [] {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tile_pap, kT, 0));
+        return static_cast<unsigned>(std::min(std::max(per_sm, 1), 8) * sm_count());
+    }();
     auto one_wave = [](auto kernel) {
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kT, 0));
@@ -833,6 +878,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
                 k_spmv_bsr_pap<2><<<bsr_grid2, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
                                                            S.p, part.p);
         } else switch (lpr) {
+            case 1: k_spmv_tile_pap<<<tgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             case 9: k_spmv_pap<8, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;

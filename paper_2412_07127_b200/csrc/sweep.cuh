@@ -66,6 +66,80 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp,
     return group_sum<LPR>(acc);
 }
 
+// Short scalar rows (7-point stencils): a warp takes 32 consecutive rows,
+// whose entries are one contiguous range. The lanes stream that range with
+// coalesced index / value loads (kTileU per lane issued before the gathers),
+// stage the products in shared memory, and then each lane adds up its own
+// row in CSR order starting from 0 — the reference's csr_matvec
+// (sparse.cpp:121-135: acc += v * x, unfused) bit for bit. Ranges longer
+// than the stage run in chunks; the per-row order is unchanged.
+// measured on the 256^3 7-point product (stand-alone, L2 flushed):
+// U = 10 at 5 CTAs/SM 0.356 ms; U = 8: 0.371; U = 12 / 16 at 4 CTAs/SM
+// 0.399 / 0.411; U = 6 at 6 CTAs/SM 0.558; lane 31's end pointer through a
+// shuffle instead of a second load 0.494
+#ifndef TILE_U
+#define TILE_U 10
+#endif
+#ifndef TILE_SPAN_SHFL
+#define TILE_SPAN_SHFL 0
+#endif
+#ifndef TILE_MINB
+#define TILE_MINB 5
+#endif
+#if TILE_MINB > 0
+#define TILE_LB(t) __launch_bounds__(t, TILE_MINB)
+#else
+#define TILE_LB(t) __launch_bounds__(t)
+#endif
+constexpr int kTileU = TILE_U;
+constexpr int kTileCh = 32 * kTileU;  // products staged per warp per chunk
+
+struct RowSpan {
+    int64_t b, e;
+};
+
+// lane l of a row tile: [rp[row], rp[row + 1]) (row = tile start + l)
+__device__ __forceinline__ RowSpan row_span(const int64_t* __restrict__ rp, int64_t n, int64_t row) {
+#if TILE_SPAN_SHFL
+    const int lane = threadIdx.x & 31;
+    const int64_t b = __ldg(rp + (row < n ? row : n));
+    int64_t e = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) e = __ldg(rp + (row + 1 < n ? row + 1 : n));
+    return RowSpan{b, e};
+#else
+    return RowSpan{__ldg(rp + (row < n ? row : n)), __ldg(rp + (row + 1 < n ? row + 1 : n))};
+#endif
+}
+
+__device__ __forceinline__ double tile_rows_dot(const RowSpan& s, const int32_t* __restrict__ cols,
+                                                const double* __restrict__ vals, const double* __restrict__ x,
+                                                double* sh, int lane) {
+    const int64_t base = __shfl_sync(0xffffffffu, s.b, 0);
+    const int64_t end = __shfl_sync(0xffffffffu, s.e, 31);
+    double acc = 0.0;
+    for (int64_t c0 = base; c0 < end; c0 += kTileCh) {
+        const int cnt = static_cast<int>(end - c0 < kTileCh ? end - c0 : kTileCh);
+        int32_t j[kTileU];
+        double v[kTileU];
+#pragma unroll
+        for (int u = 0; u < kTileU; ++u) {
+            const int k = lane + 32 * u;
+            j[u] = k < cnt ? __ldg(cols + (c0 + k)) : 0;
+            v[u] = k < cnt ? __ldg(vals + (c0 + k)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kTileU; ++u) {
+            const int k = lane + 32 * u;
+            if (k < cnt) sh[k] = __dmul_rn(v[u], __ldg(x + j[u]));
+        }
+        __syncwarp();
+        const int64_t kb = s.b > c0 ? s.b : c0, ke = s.e < c0 + cnt ? s.e : c0 + cnt;
+        for (int64_t k = kb; k < ke; ++k) acc = __dadd_rn(acc, sh[k - c0]);
+        __syncwarp();
+    }
+    return acc;
+}
+
 // Row pointers of block row b (node-blocked product), loaded one row ahead.
 template <int BS>
 struct BsrRow {

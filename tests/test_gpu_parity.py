@@ -202,6 +202,40 @@ def test_spmv_and_sweeps_match_oracle():
         assert np.linalg.norm(yt.cpu().numpy() - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
+def _seq_matvec(rp, cols, vals, x):
+    y = np.empty(len(rp) - 1)
+    for i in range(len(rp) - 1):
+        acc = 0.0
+        for k in range(rp[i], rp[i + 1]):
+            acc = acc + vals[k] * x[cols[k]]
+        y[i] = acc
+    return y
+
+
+def test_short_row_spmv_bit_exact():
+    """Short scalar rows run the row-tile product (a warp per 32 rows,
+    products staged, each row summed from 0 in CSR order, unfused): the
+    reference's csr_matvec (sparse.cpp:121-135) bit for bit — also across
+    empty rows and a row longer than one staging chunk."""
+    import torch
+    rng = np.random.default_rng(7)
+    n = 3000
+    lens = rng.integers(0, 9, n)
+    lens[100], lens[2999] = 700, 300
+    lens[2000:2040] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    cases = [P.Matrix.gen_poisson(2, 40), P.Matrix.gen_diffusion(3, 13, -3.0, 3.0, 4),
+             P.Matrix.from_csr(rp, cols, rng.standard_normal(int(rp[-1])))]
+    for a in cases:
+        arp, acols, avals = a.csr()
+        x = rng.standard_normal(a.n)
+        xt = torch.from_numpy(x).cuda()
+        yt = torch.empty_like(xt)
+        a.spmv_device(xt.data_ptr(), yt.data_ptr())
+        assert np.array_equal(bits(yt.cpu().numpy()), bits(_seq_matvec(arp, acols, avals, x)))
+
+
 def test_deterministic_runs():
     w = SMALL[1]
     a, b, model, *_ = built(w)
