@@ -121,6 +121,7 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "sm_min_mhz": float(np.min(sm)) if sm else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -317,6 +318,7 @@ def run_b200(args, w):
                        "iterations": r0["iterations"], "converged": r0["converged"],
                        "time_to_tol_s": ms / args.steps / 1e3, "p_time_s": r0["p_time"],
                        "analysis_s": r0["analysis_time"], "ic0_s": r0["ic0_time"], "cg_s": r0["cg_time"],
+                       "cg_s_per_step": [round(r["cg_time"], 4) for r in reps],
                        "true_rel_residual": r0["true_rel_residual"], "block_size": info["block_size"],
                        "levels": [info["block_levels_lower"], info["block_levels_upper"]]},
             "roofline": roofline,

@@ -661,6 +661,13 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     rep.gnn_time = pc.ms_gnn / 1e3;
     const bool factor = pc.kind == Kind::IC0 || pc.kind == Kind::NIC || pc.kind == Kind::GnnIC;
     Timer cg(st);
+    const auto h0 = std::chrono::steady_clock::now();
+    static const bool gtrace = getenv("PCLAB_PCG_TRACE") != nullptr;
+    auto trace = [&](const char* what) {
+        if (gtrace)
+            fprintf(stderr, "solve %s at %.3f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    };
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     const int parts_max = sm_count() * 8;
     DevBuf<Scal> S(1);
@@ -701,6 +708,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         rep.true_rel_residual = 1.0;
         return rep;
     }
+    trace("setup");
     const Analysis* an = factor ? a.an.get() : nullptr;
     // backward sweep fused with the product (node-blocked matrices)
     const bool fused = an && an->fused_up;
@@ -906,8 +914,14 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         mark();
     };
     auto iteration = [&](double* pold, double* pnew) { iteration_parts(pold, pnew, [] {}); };
-    int* hdone = nullptr;
-    CK(cudaMallocHost(&hdone, sizeof(int)));
+    // pinned done flag, allocated once per host thread: a pinned allocation
+    // inside the timed solve could stall the host (page pinning) while the
+    // GPU idles
+    thread_local int* hdone = [] {
+        int* h = nullptr;
+        CK(cudaMallocHost(&h, sizeof(int)));
+        return h;
+    }();
     if (prof_ms) {
         seq_side = true;  // the side kernel in stream order: its own slot
         // eager iterations with an event between kernels: per-kernel device
@@ -961,11 +975,12 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         }
         join_side();  // the side stream rejoins before the capture ends
         CK(cudaStreamEndCapture(st, &graph));
+        trace("captured");
         CK(cudaGraphInstantiate(&exec, graph, 0));
+        trace("instantiated");
         size_t nodes = 0;
         CK(cudaGraphGetNodes(graph, nullptr, &nodes));
         g_launches = before;  // captured launches are counted per replay below
-        static const bool gtrace = getenv("PCLAB_PCG_TRACE") != nullptr;
         for (;;) {
             const auto t0 = std::chrono::steady_clock::now();
             CK(cudaGraphLaunch(exec, st));
@@ -983,7 +998,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     join_side();
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
-    cudaFreeHost(hdone);
+    trace("loop done");
     rep.cg_time = cg.ms() / 1e3;
     CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
