@@ -80,9 +80,6 @@ __device__ __forceinline__ double row_dot(const int64_t* __restrict__ rp,
 #ifndef TILE_U
 #define TILE_U 10
 #endif
-#ifndef TILE_SPAN_SHFL
-#define TILE_SPAN_SHFL 0
-#endif
 #ifndef TILE_MINB
 #define TILE_MINB 5
 #endif
@@ -100,15 +97,7 @@ struct RowSpan {
 
 // lane l of a row tile: [rp[row], rp[row + 1]) (row = tile start + l)
 __device__ __forceinline__ RowSpan row_span(const int64_t* __restrict__ rp, int64_t n, int64_t row) {
-#if TILE_SPAN_SHFL
-    const int lane = threadIdx.x & 31;
-    const int64_t b = __ldg(rp + (row < n ? row : n));
-    int64_t e = __shfl_down_sync(0xffffffffu, b, 1);
-    if (lane == 31) e = __ldg(rp + (row + 1 < n ? row + 1 : n));
-    return RowSpan{b, e};
-#else
     return RowSpan{__ldg(rp + (row < n ? row : n)), __ldg(rp + (row + 1 < n ? row + 1 : n))};
-#endif
 }
 
 __device__ __forceinline__ double tile_rows_dot(const RowSpan& s, const int32_t* __restrict__ cols,
