@@ -251,9 +251,7 @@ def run_b200(args, w):
     hbm, peak_kind = peaks()
     lay = pc.layout()
     kern = T.iteration_kernels(pc, n, nnz, prof)
-    if prof["fused"]:
-        top, top_name = "sweep_upper_spmv", "bsr_upper_mv_kernel (fused sweep + product)"
-    elif lay["node_blocked"]:
+    if lay["node_blocked"]:
         top, top_name = "sweep_lower", "bsr_trsv_kernel (node-blocked sweep)"
     else:
         top, top_name = "sweep_lower", "rr_trsv_kernel (lower sweep)"

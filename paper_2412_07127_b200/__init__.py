@@ -374,13 +374,11 @@ class Precond:
         _check(lib().pclab_trsv_device(self._h, int(upper), b_ptr, x_ptr, stream or None))
 
     def profile_device(self, b_ptr: int, x_ptr: int, iters: int) -> dict:
-        """Per-kernel device ms of the PCG loop (eager iterations). With the
-        fused backward sweep (node-blocked matrices) the product A z is part
-        of `sweep_upper_ms` and `spmv_ms` is the p/q update."""
+        """Per-kernel device ms of the PCG loop (eager iterations)."""
         t = np.zeros(8)
         _check(lib().pclab_pcg_profile(self.matrix.handle, self._h, b_ptr, x_ptr, iters, t))
         return {"spmv_ms": t[0], "axpy_ms": t[1], "sweep_lower_ms": t[2], "sweep_upper_ms": t[3],
-                "dot_ms": t[4], "iterations": int(t[5]), "fused": bool(t[6])}
+                "dot_ms": t[4], "iterations": int(t[5])}
 
     def solve_device(self, b_ptr: int, x_ptr: int, rel_tol: float = 1e-6, max_iters: int = -1,
                      record_history: bool = False, stream: int = 0) -> dict:

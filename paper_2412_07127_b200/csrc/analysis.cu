@@ -122,19 +122,6 @@ __global__ void bsr_check_full(int64_t nb, int bs, const int64_t* __restrict__ a
     }
 }
 
-// Key of A block row b for the fused product: the highest backward-sweep
-// level among its column blocks (when its last z input is published).
-__global__ void mv_keys(int64_t nb, int bs, const int32_t* __restrict__ lev, const int64_t* __restrict__ arp,
-                        const int32_t* __restrict__ acols, int32_t* __restrict__ key, int32_t* __restrict__ val) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b >= nb) return;
-    int lm = 0;
-    const int64_t r = b * bs;
-    for (int64_t k = arp[r]; k < arp[r + 1]; k += bs) lm = max(lm, lev[acols[k] / bs]);
-    key[b] = lm;
-    val[b] = static_cast<int32_t>(b);
-}
-
 // Level sets by Kahn layering on the block DAG: a block's level is one
 // more than the largest level among its predecessors, so releasing a block
 // when its last predecessor is processed assigns exactly that level (the
@@ -435,77 +422,6 @@ __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* 
     }
 }
 
-// ---------------------------------------------------------------- tiles
-// Owner of block b: piece floor(b * P / nb) (contiguous ranges), piece k
-// runs on CTA k % C.
-__device__ __forceinline__ int64_t tile_owner(int64_t b, int64_t nb, int64_t P, int C) {
-    return (b * P / nb) % C;
-}
-
-__global__ void tile_keys(int64_t nb, int64_t P, int C, const int32_t* __restrict__ level,
-                          unsigned long long* __restrict__ key) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b >= nb) return;
-    key[b] = (static_cast<unsigned long long>(tile_owner(b, nb, P, C)) << 42) |
-             (static_cast<unsigned long long>(level[b]) << 22) | static_cast<unsigned long long>(b);
-}
-
-// run = one (owner, level) group of the sorted keys
-__global__ void tile_run_flags(int64_t nb, const unsigned long long* __restrict__ skey, int64_t* __restrict__ flag) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (s >= nb) return;
-    flag[s] = (s == 0 || (skey[s] >> 22) != (skey[s - 1] >> 22)) ? 1 : 0;
-}
-
-__global__ void tile_run_first(int64_t nb, const int64_t* __restrict__ flag, const int64_t* __restrict__ runincl,
-                               int64_t* __restrict__ first) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (s >= nb) return;
-    if (flag[s]) first[runincl[s] - 1] = s;
-    if (s == nb - 1) first[runincl[s]] = nb;
-}
-
-// padded run lengths (whole warp items of G blocks), in place of the next
-// run's first index shifted by one: len[r] for r < nruns, 0 at nruns
-__global__ void tile_run_len(int64_t nruns, int G, const int64_t* __restrict__ first, int64_t* __restrict__ plen) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r > nruns) return;
-    plen[r] = r < nruns ? (first[r + 1] - first[r] + G - 1) / G * G : 0;
-}
-
-__global__ void tile_place(int64_t nb, const unsigned long long* __restrict__ skey, const int64_t* __restrict__ runincl,
-                           const int64_t* __restrict__ first, const int64_t* __restrict__ rpos,
-                           int32_t* __restrict__ slots, int64_t* __restrict__ posof, int64_t* __restrict__ tbeg) {
-    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (s >= nb) return;
-    const int64_t r = runincl[s] - 1;
-    const int64_t pos = rpos[r] + (s - first[r]);
-    const int64_t b = static_cast<int64_t>(skey[s] & ((1ULL << 22) - 1));
-    slots[pos] = static_cast<int32_t>(b);
-    posof[b] = pos;
-    const unsigned long long own = skey[s] >> 42;
-    if (s == 0 || own != (skey[s - 1] >> 42)) tbeg[own] = pos;
-}
-
-__global__ void tile_local(int64_t nb, int64_t P, int C, const int64_t* __restrict__ tbeg, int64_t* __restrict__ posof) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b < nb) posof[b] -= tbeg[tile_owner(b, nb, P, C)];
-}
-
-__global__ void tile_cols(int64_t nb, int bs, int64_t P, int C, const int64_t* __restrict__ bp,
-                          const int32_t* __restrict__ bcol, const int64_t* __restrict__ posof,
-                          uint32_t* __restrict__ tcol) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b >= nb) return;
-    const int64_t ob = tile_owner(b, nb, P, C);
-    for (int64_t k = bp[b]; k < bp[b + 1]; ++k) {
-        const int64_t nbr = bcol[k] / bs;
-        int64_t d = tile_owner(nbr, nb, P, C) == ob ? posof[b] - posof[nbr] : 0;
-        if (d <= 0 || d >= (1 << kTileDistBits)) d = 0;
-        tcol[k] = (static_cast<uint32_t>(nbr) << kTileDistBits) | static_cast<uint32_t>(d);
-    }
-}
-
 template <class T>
 T dev_read(const T* d, cudaStream_t st) {
     T v;
@@ -676,216 +592,6 @@ static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, c
 }
 
 
-// Tiled schedule of a node-blocked sweep (TileSched): `ntiles` CTAs,
-// `per_cta` contiguous pieces each. Needs < 2^22 blocks and < 2^20 levels
-// (key packing); returns false (no tile schedule) otherwise.
-static bool build_tiles(const DevCsr& M, const BlockCols& bc, Schedule& s, int ntiles, int per_cta,
-                        cudaStream_t st) {
-    TileSched& t = s.tile;
-    const int64_t nb = s.nblocks;
-    const int G = s.per_item;
-    if (nb == 0 || nb >= (1LL << 22) || s.nlevels >= (1 << 20)) return false;
-    const int C = static_cast<int>(std::min<int64_t>(ntiles, nb));
-    const int64_t P = std::min<int64_t>(static_cast<int64_t>(C) * std::max(per_cta, 1), nb);
-    t.ntiles = C;
-    t.pieces = P;
-    DevBuf<unsigned long long> key(nb), skey(nb);
-    tile_keys<<<grid_for(nb, 256), 256, 0, st>>>(nb, P, C, s.level.p, key.p);
-    CK_LAUNCH();
-    {
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, tmp, key.p, skey.p, static_cast<int>(nb), 0, 64, st);
-        DevBuf<unsigned char> tb(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceRadixSort::SortKeys(tb.p, tmp, key.p, skey.p, static_cast<int>(nb), 0, 64, st);
-        CK(cudaStreamSynchronize(st));
-    }
-    DevBuf<int64_t> flag(nb), runincl(nb);
-    tile_run_flags<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, flag.p);
-    CK_LAUNCH();
-    {
-        size_t tmp = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tmp, flag.p, runincl.p, nb, st);
-        DevBuf<unsigned char> tb(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceScan::InclusiveSum(tb.p, tmp, flag.p, runincl.p, nb, st);
-    }
-    const int64_t nruns = dev_read(runincl.p + nb - 1, st);
-    DevBuf<int64_t> first(nruns + 1), rpos(nruns + 1);
-    tile_run_first<<<grid_for(nb, 256), 256, 0, st>>>(nb, flag.p, runincl.p, first.p);
-    CK_LAUNCH();
-    tile_run_len<<<grid_for(nruns + 1, 256), 256, 0, st>>>(nruns, G, first.p, rpos.p);
-    CK_LAUNCH();
-    scan_inplace(rpos.p, nruns + 1, st);
-    t.npos = dev_read(rpos.p + nruns, st);
-    t.slots.alloc(t.npos);
-    t.tbeg.alloc(C + 1);
-    CK(cudaMemsetAsync(t.slots.p, 0xff, sizeof(int32_t) * t.npos, st));
-    CK(cudaMemcpyAsync(t.tbeg.p + C, &t.npos, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    DevBuf<int64_t> posof(nb);
-    tile_place<<<grid_for(nb, 256), 256, 0, st>>>(nb, skey.p, runincl.p, first.p, rpos.p, t.slots.p, posof.p,
-                                                  t.tbeg.p);
-    CK_LAUNCH();
-    tile_local<<<grid_for(nb, 256), 256, 0, st>>>(nb, P, C, t.tbeg.p, posof.p);
-    CK_LAUNCH();
-    t.tcol.alloc(std::max<int64_t>(bc.bcol.n, 1));
-    tile_cols<<<grid_for(nb, 256), 256, 0, st>>>(nb, s.bs, P, C, bc.bp.p, bc.bcol.p, posof.p, t.tcol.p);
-    CK_LAUNCH();
-    DevBuf<int> bad(1);
-    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-    t.srp.alloc(4 * t.npos);
-    slot_rp_fill<<<grid_for(t.npos, 256), 256, 0, st>>>(t.npos, s.bs, t.slots.p, M.rp.p, bc.bp.p, t.srp.p, bad.p);
-    CK_LAUNCH();
-    if (dev_read(bad.p, st) != 0) {
-        t = TileSched{};
-        return false;
-    }
-    return true;
-}
-
-// ---------------------------------------------------------------- chains
-// Sweep-order index r of block b: lower sweeps run b = r, upper b = nb-1-r.
-// A block continues the chain of the block before it (in sweep order) when
-// that block is one of its neighbours: the last block column of an L block
-// row, the first of a U block row.
-__global__ void chain_starts(int64_t nb, int bs, bool upper, const int64_t* __restrict__ bp,
-                             const int32_t* __restrict__ bcol, int64_t* __restrict__ cs) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r >= nb) return;
-    const int64_t b = upper ? nb - 1 - r : r;
-    bool cont = false;
-    if (r > 0 && bp[b + 1] > bp[b]) {
-        const int64_t prev = upper ? b + 1 : b - 1;
-        const int32_t c = upper ? bcol[bp[b]] : bcol[bp[b + 1] - 1];
-        cont = static_cast<int64_t>(c) == prev * bs;
-    }
-    cs[r] = cont ? -1 : r;
-}
-
-struct MaxOp {
-    __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
-};
-
-__global__ void seg_start_flags(int64_t nb, int k, const int64_t* __restrict__ cs, int64_t* __restrict__ flag) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r < nb) flag[r] = ((r - cs[r]) % k) == 0 ? 1 : 0;
-}
-
-// segment s starts at sweep index start[s]; key = (level of its first block, r)
-__global__ void seg_make(int64_t nb, bool upper, const int64_t* __restrict__ flag_incl,
-                         const int32_t* __restrict__ level, int64_t* __restrict__ start,
-                         unsigned long long* __restrict__ key, int32_t* __restrict__ sid) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r >= nb) return;
-    if (r == 0 || flag_incl[r] != flag_incl[r - 1]) {
-        const int64_t s = flag_incl[r] - 1;
-        start[s] = r;
-        const int64_t b = upper ? nb - 1 - r : r;
-        key[s] = (static_cast<unsigned long long>(level[b]) << 32) | static_cast<unsigned long long>(r);
-        sid[s] = static_cast<int32_t>(s);
-    }
-}
-
-// slots of the sorted segments; item of every block
-__global__ void seg_slots_fill(int64_t nseg, int64_t nb, int G, bool upper, const int32_t* __restrict__ sorted,
-                               const int64_t* __restrict__ start, int32_t* __restrict__ sfirst,
-                               int32_t* __restrict__ slen, int32_t* __restrict__ item_of) {
-    const int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (pos >= nseg) return;
-    const int32_t s = sorted[pos];
-    const int64_t r0 = start[s], r1 = s + 1 < nseg ? start[s + 1] : nb;
-    sfirst[pos] = static_cast<int32_t>(upper ? nb - 1 - r0 : r0);
-    slen[pos] = static_cast<int32_t>(r1 - r0);
-    for (int64_t r = r0; r < r1; ++r) item_of[upper ? nb - 1 - r : r] = static_cast<int32_t>(pos / G);
-}
-
-__global__ void chain_window(int64_t nb, int bs, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
-                             const int32_t* __restrict__ bcol, const int32_t* __restrict__ item_of,
-                             unsigned long long* __restrict__ fwd, unsigned* __restrict__ maxnb,
-                             unsigned* __restrict__ maxblk) {
-    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (b >= nb) return;
-    long long f = 0;
-    for (int64_t k = bp[b]; k < bp[b + 1]; ++k) f = max(f, static_cast<long long>(item_of[bcol[k] / bs]) - item_of[b]);
-    atomicMax(fwd, static_cast<unsigned long long>(f));
-    atomicMax(maxnb, static_cast<unsigned>(bp[b + 1] - bp[b]));
-    atomicMax(maxblk, static_cast<unsigned>(rp[(b + 1) * bs] - rp[b * bs]));
-}
-
-static void build_chains(const DevCsr& M, const BlockCols& bc, int bs, bool upper, int k, Schedule& s,
-                         cudaStream_t st) {
-    const int64_t nb = s.nblocks;
-    s.chain_k = k;
-    if (nb == 0) return;
-    DevBuf<int64_t> cs(nb), flag(nb);
-    chain_starts<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, upper, bc.bp.p, bc.bcol.p, cs.p);
-    CK_LAUNCH();
-    {
-        size_t tmp = 0;
-        cub::DeviceScan::InclusiveScan(nullptr, tmp, cs.p, cs.p, MaxOp(), nb, st);
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceScan::InclusiveScan(t.p, tmp, cs.p, cs.p, MaxOp(), nb, st);
-    }
-    seg_start_flags<<<grid_for(nb, 256), 256, 0, st>>>(nb, k, cs.p, flag.p);
-    CK_LAUNCH();
-    {
-        size_t tmp = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tmp, flag.p, flag.p, nb, st);
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceScan::InclusiveSum(t.p, tmp, flag.p, flag.p, nb, st);
-    }
-    const int64_t nseg = dev_read(flag.p + nb - 1, st);
-    s.nseg = nseg;
-    DevBuf<int64_t> start(nseg);
-    DevBuf<unsigned long long> key(nseg), skey(nseg);
-    DevBuf<int32_t> sid(nseg), sorted(nseg);
-    seg_make<<<grid_for(nb, 256), 256, 0, st>>>(nb, upper, flag.p, s.level.p, start.p, key.p, sid.p);
-    CK_LAUNCH();
-    {
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, sid.p, sorted.p, static_cast<int>(nseg), 0, 64,
-                                        st);
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, sid.p, sorted.p, static_cast<int>(nseg), 0, 64, st);
-    }
-    const int G = 1;  // one segment per warp (chain_trsv_kernel)
-    s.chain_items = (nseg + G - 1) / G;
-    s.seg_first.alloc(s.chain_items * G);
-    s.seg_len.alloc(s.chain_items * G);
-    CK(cudaMemsetAsync(s.seg_first.p, 0xff, sizeof(int32_t) * s.chain_items * G, st));
-    CK(cudaMemsetAsync(s.seg_len.p, 0, sizeof(int32_t) * s.chain_items * G, st));
-    DevBuf<int32_t> item_of(nb);
-    seg_slots_fill<<<grid_for(nseg, 256), 256, 0, st>>>(nseg, nb, G, upper, sorted.p, start.p, s.seg_first.p,
-                                                        s.seg_len.p, item_of.p);
-    CK_LAUNCH();
-    DevBuf<unsigned long long> fwd(1);
-    DevBuf<unsigned> mnb(2);
-    CK(cudaMemsetAsync(fwd.p, 0, sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(mnb.p, 0, 2 * sizeof(unsigned), st));
-    chain_window<<<grid_for(nb, 256), 256, 0, st>>>(nb, bs, M.rp.p, bc.bp.p, bc.bcol.p, item_of.p, fwd.p, mnb.p,
-                                                    mnb.p + 1);
-    CK_LAUNCH();
-    s.chain_maxfwd = static_cast<int64_t>(dev_read(fwd.p, st));
-    s.chain_maxnb = static_cast<int32_t>(dev_read(mnb.p, st));
-    s.chain_maxblk = static_cast<int32_t>(dev_read(mnb.p + 1, st));
-}
-
-// A block rows sorted by the backward-sweep level that completes their z
-// inputs (Analysis::mv_order).
-static void build_mv_order(const DevCsr& A, Analysis& an, cudaStream_t st) {
-    const Schedule& up = an.blk_up;
-    const int64_t nb = up.nblocks;
-    an.mv_order.alloc(std::max<int64_t>(nb, 1));
-    if (nb == 0) return;
-    DevBuf<int32_t> key(nb), skey(nb), val(nb);
-    mv_keys<<<grid_for(nb, 256), 256, 0, st>>>(nb, an.bs, up.level.p, A.rp.p, A.cols.p, key.p, val.p);
-    CK_LAUNCH();
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, val.p, an.mv_order.p, static_cast<int>(nb), 0, 32,
-                                    st);
-    DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-    cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, val.p, an.mv_order.p, static_cast<int>(nb), 0, 32, st);
-    CK(cudaStreamSynchronize(st));
-}
-
 Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     if (m.an) return *m.an;
     const DevCsr& a = m.a;
@@ -959,13 +665,10 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     int lanes = 2;
     while (lanes < 32 && lanes < work) lanes *= 2;
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
-    // (row-granular level sets are computed on request only: pclab_precond_levels)
-    // the critical-predecessor poll is the entry-lane sweep's (and traces')
-    // (round-robin sweeps need the slot records; PCLAB_RR=0 selects the
-    // claim-based entry-lane sweep for matrices that are not node-blocked)
-    static const bool rr_on = !(getenv("PCLAB_RR") && atoi(getenv("PCLAB_RR")) == 0);
-    an->blk_lo.need_crit = an->blk_up.need_crit =
-        (!an->bsr && !rr_on) || getenv("PCLAB_TRSV_TRACE") != nullptr;
+    // (row-granular level sets are computed on request only: pclab_precond_levels;
+    // the critical-predecessor index is needed by the claim-based fallback
+    // sweep only, filled below when the round-robin slot records do not fit)
+    an->blk_lo.need_crit = an->blk_up.need_crit = false;
     if (an->bsr) {  // block columns first: the levelling walks them
         build_block_cols(L, bs, 0, an->lbc, st);
         build_block_cols(U, bs, 1, an->ubc, st);
@@ -977,7 +680,7 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     an->rr = false;
     DevBuf<int> bad(1);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-    if (an->bsr || rr_on) {
+    {
         for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
             const bool lo = sc == &an->blk_lo;
             const DevCsr& M = lo ? L : U;
@@ -1004,16 +707,6 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
         }
     }
     if (an->bsr) {
-        // chain-segment sweep (chain.cuh): opt-in with PCLAB_CHAIN=1. On
-        // configs[2] it is slower than the round-robin node-blocked sweep
-        // (1.34 vs 0.99 ms): in-segment steps still pay an L2 re-poll for
-        // the just-in-time cross-segment dependencies
-        static const int chain_k = getenv("PCLAB_CHAIN_K") ? atoi(getenv("PCLAB_CHAIN_K")) : 128;
-        static const bool chain_on = getenv("PCLAB_CHAIN") && atoi(getenv("PCLAB_CHAIN")) != 0;
-        if (chain_on && chain_k > 0) {
-            build_chains(L, an->lbc, bs, false, chain_k, an->blk_lo, st);
-            build_chains(U, an->ubc, bs, true, chain_k, an->blk_up, st);
-        }
         if (dev_read(bad.p, st) != 0) {  // a row too long for the packed record: entry-lane sweep
             an->bsr = false;
             for (Schedule* sc : {&an->blk_lo, &an->blk_up}) {
@@ -1027,21 +720,6 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
             }
         }
     }
-    // tiled node-blocked sweeps (opt-in, PCLAB_TILE=1): one CTA per SM owns
-    // contiguous block ranges (PCLAB_TILE_K pieces per CTA, PCLAB_TILES
-    // CTAs). On configs[2] slower than the round-robin sweep (1.11 vs 1.03 ms
-    // at 32-64 pieces per CTA, 2.7 ms at 1): the shared-memory handoff saves
-    // little because the sweep is bound by its load stream, not the L2 hop
-    if (an->bsr) {
-        static const bool tile_on = getenv("PCLAB_TILE") && atoi(getenv("PCLAB_TILE")) != 0;
-        static const int tile_k = getenv("PCLAB_TILE_K") ? atoi(getenv("PCLAB_TILE_K")) : 1;
-        static const int tiles = getenv("PCLAB_TILES") ? atoi(getenv("PCLAB_TILES")) : 0;
-        if (tile_on) {
-            const int C = tiles > 0 ? std::min(tiles, sm_count()) : sm_count();
-            build_tiles(L, an->lbc, an->blk_lo, C, tile_k, st);
-            build_tiles(U, an->ubc, an->blk_up, C, tile_k, st);
-        }
-    }
     // node-blocked A: the PCG product reads one column index per block
     an->a_bsr = false;
     if (an->bsr) {
@@ -1053,14 +731,6 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
             build_block_cols(a, bs, 2, an->abc, st);
             an->a_bsr = true;
         }
-    }
-    // upper sweep fused with the next iteration's A z (node-blocked A).
-    // Opt-in (PCLAB_FUSE=1): on configs[2] the product CTAs slow the sweep
-    // more than the separate SpMV costs (2.37 vs 1.02 + 1.04 ms)
-    an->fused_up = false;
-    if (an->a_bsr && getenv("PCLAB_FUSE") && atoi(getenv("PCLAB_FUSE")) != 0) {
-        build_mv_order(a, *an, st);
-        an->fused_up = true;
     }
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));

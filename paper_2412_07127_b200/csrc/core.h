@@ -64,25 +64,6 @@ struct DevCsr {
     DevBuf<double> vals;
 };
 
-// Tiled schedule of a node-blocked sweep (tile_trsv_kernel): the block
-// rows are cut into `pieces` contiguous ranges, piece k owned by CTA
-// k % ntiles. Each CTA runs its blocks in (level, index) order -- its list
-// is positions [tbeg[c], tbeg[c+1]), every level's run padded to whole
-// warp items -- and hands results to its own later blocks through a
-// shared-memory ring; only dependencies owned by another CTA go through
-// L2. Contiguous ranges make the cross-CTA dependencies one-directional.
-struct TileSched {
-    int ntiles = 0;
-    int64_t pieces = 0;
-    int64_t npos = 0;
-    DevBuf<int64_t> tbeg;   // [ntiles + 1] first position of each CTA's list
-    DevBuf<int32_t> slots;  // [npos] block at each position, -1 = padding
-    DevBuf<int32_t> srp;    // [4 * npos] slot records (as Schedule::slot_rp)
-    DevBuf<uint32_t> tcol;  // [block columns] (neighbour block << 10) | d, d = distance
-                            // back in the owner's list (1..1023) when the owner is
-                            // the same CTA, else 0 (read from L2)
-};
-
 // Dependency schedule of a triangular sweep over blocks of `bs`
 // consecutive rows: blocks sorted by (level, index) and cut into warp
 // items of at most `per_item` blocks of one level.
@@ -102,18 +83,7 @@ struct Schedule {
     DevBuf<int32_t> slots;       // [nitems * per_item] block per lane group, -1 idle
     DevBuf<int32_t> slot_rp;     // [nitems * per_item * 4] 16-byte slot records {block (-1 idle),
                                  //  first row pointer, first block column, row lengths 10 bits each}
-    // chain segments (node-blocked sweeps): runs of consecutive blocks where
-    // each depends on the one before it in sweep order, cut at chain_k
-    // blocks, sorted by (level of the first block, index), one per warp
-    int64_t nseg = 0, chain_items = 0;
-    int chain_k = 0;
-    int64_t chain_maxfwd = -1;    // max (item of a dependency - item of the block)
-    int32_t chain_maxnb = 0;      // most neighbour blocks of one block
-    int32_t chain_maxblk = 0;     // most factor entries of one block (all its rows)
-    DevBuf<int32_t> seg_first;    // [chain_items] first block
-    DevBuf<int32_t> seg_len;      // [chain_items]
     int64_t max_level_width = 0;
-    TileSched tile;               // built for node-blocked sweeps (tile_trsv_kernel)
 };
 
 // Block-column view of a node-blocked CSR matrix (Analysis::bsr): block
@@ -143,10 +113,6 @@ struct Analysis {
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)
-    // backward sweep fused with w = A z (node-blocked A): the A block rows
-    // in the order their z inputs complete (max upper level over the row)
-    bool fused_up = false;
-    DevBuf<int32_t> mv_order;
     double ms = 0.0;         // wall time of the analysis (CUDA events)
     uint64_t id = 0;         // unique per analysis (IC(0) mask cache key)
 };
@@ -222,14 +188,8 @@ void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* ou
 void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
 void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
           cudaStream_t st);
-struct RUpdate;  // sweep.cuh: forward sweep fused with r_new = r - alpha q
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
-                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false,
-                 const RUpdate* ru = nullptr);
-// Backward sweep z = U^-1 y fused with w = A z (Analysis::fused_up).
-void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
-                       const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
-                       cudaStream_t st);
+                 double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false);
 void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);
 int spmv_lanes(const Matrix& a);
 void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st);

@@ -6,7 +6,6 @@
 #include <string>
 #include <vector>
 
-#include "chain.cuh"
 #include "core.h"
 #include "sweep.cuh"
 
@@ -233,143 +232,61 @@ void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaSt
     CK_LAUNCH();
 }
 
-// Developer knob: PCLAB_TRSV_TUNE = mode | (sleep_ns << 8); mode 0 polls the
-// critical predecessor first, mode 1 polls every dependency directly.
-static int trsv_tune() {
-    static const int t = getenv("PCLAB_TRSV_TUNE") ? atoi(getenv("PCLAB_TRSV_TUNE")) : 0;
-    return t;
-}
-// Developer trace (PCLAB_TRSV_TRACE=<file>): per-item globaltimer stamps of
-// the stand-alone sweep, written as int64 [nitems x 4].
-static long long* g_trace = nullptr;
-
 // Resident warps for a sweep: enough to hold a few levels of items in
 // flight (loads stream while the frontier advances) but not so many that
 // idle pollers crowd L2.
 // Measured on configs[2]: 4 levels for the entry-lane sweep, 2 for the
 // node-blocked one (its pollers read BS values each, 1.40 vs 1.65 ms at 4).
-static unsigned trsv_grid(const Schedule& s, double depth_default, int warps_per_cta = 8) {
+static unsigned trsv_grid(const Schedule& s, double depth, int warps_per_cta = 8) {
     const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
-    static const double env_depth = getenv("PCLAB_TRSV_DEPTH") ? atof(getenv("PCLAB_TRSV_DEPTH")) : 0.0;
-    const double depth = env_depth > 0 ? env_depth : depth_default;
     const int64_t warps = static_cast<int64_t>(depth * per_level) + 1;
     const int64_t blocks = (warps + warps_per_cta - 1) / warps_per_cta;
     return static_cast<unsigned>(
         std::min<int64_t>(std::max<int64_t>(blocks, sm_count()), sm_count() * (64 / warps_per_cta)));
 }
 
+// Claim-based entry-lane sweep: the fallback for rows longer than the
+// round-robin sweeps' packed slot records allow (1023 entries).
 template <int LG, int BS, bool UP>
 static void launch_trsv_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd,
                           const double* b, double* x, double* reset, const int* done, unsigned* ctr,
                           cudaStream_t st) {
     trsv_kernel<LG, BS, UP><<<trsv_grid(s, 4.0), 256, 0, st>>>(s.nitems, s.slots.p, s.crit.p, M.rp.p, M.cols.p,
-                                                          vals, invd, b, x, reset, done, ctr, trsv_tune(),
-                                                          g_trace);
-}
-
-// Chain sweep (opt-in, PCLAB_CHAIN=1): used when the window condition holds
-// for the warps that fit (Schedule::chain_maxfwd < resident warps) and every
-// block has at most 32 neighbour blocks.
-template <int BS, bool UP>
-static bool launch_chain_t(const Schedule& s, const BlockCols& bc, const DevCsr& M, const double* vals,
-                           const double* invd, const double* b, double* x, double* reset, const int* done,
-                           cudaStream_t st) {
-    static const bool enabled = getenv("PCLAB_CHAIN") && atoi(getenv("PCLAB_CHAIN")) != 0;
-    if (!enabled || s.chain_items == 0 || s.chain_maxnb > 32 || s.chain_k > kChainMaxSeg) return false;
-    // bulk copies need 16-byte aligned sources (library buffers are)
-    for (const void* p : {static_cast<const void*>(vals), static_cast<const void*>(invd),
-                          static_cast<const void*>(b), static_cast<const void*>(bc.bcol.p)})
-        if (reinterpret_cast<uintptr_t>(p) & 15) return false;
-    const ChainLayout lay = chain_layout(BS, s.chain_maxblk, s.chain_maxnb);
-    const size_t smem = 8 * static_cast<size_t>(lay.warp_bytes);
-    if (smem > 220 * 1024) return false;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        CK(cudaFuncSetAttribute(chain_tma_kernel<BS, UP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-        smem_set = smem;
-    }
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_tma_kernel<BS, UP>, 256, smem));
-    const int64_t cap = static_cast<int64_t>(std::max(per_sm, 1)) * sm_count();
-    if (s.chain_maxfwd < 0 || s.chain_maxfwd >= cap * 8) return false;  // deadlock-freedom window
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(cap, (s.chain_items + 7) / 8));
-    chain_tma_kernel<BS, UP><<<grid, 256, smem, st>>>(s.chain_items, s.seg_first.p, s.seg_len.p, M.rp.p, bc.bp.p,
-                                                      bc.bcol.p, vals, invd, b, x, reset, done, lay, g_trace);
-    return true;
+                                                                vals, invd, b, x, reset, done, ctr);
 }
 
 // Round-robin items need every warp resident: the grid is capped at what
 // the GPU holds (measured best on configs[2]: as many warps as fit).
-template <int LG, int BS, bool UP, bool PAD, bool RAX, bool DEV>
+template <int LG, int BS, bool UP, bool PAD>
 static void launch_bsr_d(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, RUpdate ru) {
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st) {
     static unsigned cap = 0;
     if (!cap) {
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD, RAX, DEV>,
-                                                         BSR_THREADS, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bsr_trsv_kernel<LG, BS, UP, PAD>, BSR_THREADS, 0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
     if (s.nitems * s.per_item >= (1LL << 31)) throw DimensionError("node-blocked sweep: too many schedule slots");
     const unsigned grid = std::min(trsv_grid(s, 5.0, BSR_THREADS / 32), cap);  // ~all resident warps
-    bsr_trsv_kernel<LG, BS, UP, PAD, RAX, DEV><<<grid, BSR_THREADS, 0, st>>>(
-        s.nitems, s.slot_rp.p, bcol, vals, invd, b, x, reset, done, trsv_tune(), g_trace, ru);
-}
-
-// developer probes (PCLAB_TRSV_TUNE, PCLAB_TRSV_TRACE) select the DEV build
-template <int LG, int BS, bool UP, bool PAD, bool RAX>
-static void launch_bsr_p(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, RUpdate ru) {
-    if (trsv_tune() != 0 || g_trace != nullptr)
-        launch_bsr_d<LG, BS, UP, PAD, RAX, true>(s, bcol, vals, invd, b, x, reset, done, st, ru);
-    else
-        launch_bsr_d<LG, BS, UP, PAD, RAX, false>(s, bcol, vals, invd, b, x, reset, done, st, ru);
+    bsr_trsv_kernel<LG, BS, UP, PAD><<<grid, BSR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, bcol, vals, invd, b, x,
+                                                                   reset, done);
 }
 
 // pad: output / re-arm vectors (and the upper sweep's right-hand side)
-// stored 4 doubles per node (PCG loop, BS = 3); ru: forward sweep fused
-// with r_new = r - alpha q (PCG loop, padded)
+// stored 4 doubles per node (PCG loop, BS = 3)
 template <int LG, int BS, bool UP>
 static void launch_bsr_t(const Schedule& s, const int32_t* bcol, const double* vals, const double* invd,
-                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, bool pad,
-                         const RUpdate* ru) {
+                         const double* b, double* x, double* reset, const int* done, cudaStream_t st, bool pad) {
     if constexpr (BS == 3) {
-        if (pad && ru) {
-            if constexpr (!UP) {
-                launch_bsr_p<LG, BS, UP, true, true>(s, bcol, vals, invd, b, x, reset, done, st, *ru);
-                return;
-            }
-        } else if (pad) {
-            launch_bsr_p<LG, BS, UP, true, false>(s, bcol, vals, invd, b, x, reset, done, st, RUpdate{});
+        if (pad) {
+            launch_bsr_d<LG, BS, UP, true>(s, bcol, vals, invd, b, x, reset, done, st);
             return;
         }
     }
-    if (pad || ru) throw DimensionError("padded / fused-residual sweeps need 3x3 node blocks (forward sweep)");
-    launch_bsr_p<LG, BS, UP, false, false>(s, bcol, vals, invd, b, x, reset, done, st, RUpdate{});
+    if (pad) throw DimensionError("padded sweeps need 3x3 node blocks");
+    launch_bsr_d<LG, BS, UP, false>(s, bcol, vals, invd, b, x, reset, done, st);
 }
 
-// CTAs given to the fused product (PCLAB_MV_CTAS overrides; default two per SM)
-static unsigned mv_ctas() {
-    static const int v = getenv("PCLAB_MV_CTAS") ? atoi(getenv("PCLAB_MV_CTAS")) : 0;
-    return static_cast<unsigned>(v > 0 ? v : 2 * sm_count());
-}
-
-template <int LG, int BS>
-static void launch_fused_t(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
-                           const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
-                           cudaStream_t st) {
-    const Schedule& s = an.blk_up;
-    static const unsigned cap = resident_ctas(bsr_upper_mv_kernel<LG, BS>);
-    const unsigned nsweep = std::min(trsv_grid(s, 2.0), cap);
-    bsr_upper_mv_kernel<LG, BS><<<nsweep + mv_ctas(), 256, 0, st>>>(
-        s.nitems, s.slot_rp.p, an.ubc.bcol.p, uvals, invd, y, z, reset, nsweep, s.nblocks,
-        an.mv_order.p, A.rp.p, A.cols.p, A.vals.p, w, done, ctr, trsv_tune(), g_trace);
-}
-
-#ifndef RR_DEPTH
-#define RR_DEPTH 6.0
-#endif
 template <int LG, int BS, bool UP, int CH>
 static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, const double* invd, const double* b,
                         double* x, double* reset, const int* done, cudaStream_t st) {
@@ -379,70 +296,25 @@ static void launch_rr_t(const Schedule& s, const DevCsr& M, const double* vals, 
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rr_trsv_kernel<LG, BS, UP, CH>, RR_THREADS, 0));
         cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
     }
-    const unsigned grid = std::min(trsv_grid(s, RR_DEPTH, RR_THREADS / 32), cap);
-    if (trsv_tune() != 0)
-        rr_trsv_kernel<LG, BS, UP, CH, true><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals,
-                                                                          invd, b, x, reset, done, trsv_tune());
-    else
-        rr_trsv_kernel<LG, BS, UP, CH, false><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals,
-                                                                           invd, b, x, reset, done, 0);
-}
-
-// Tiled sweep: one 512-thread CTA per tile, all resident (1 per SM).
-// PCLAB_TILE_RING=64 selects a 64-slot ring (test knob: dependencies up to
-// 1023 positions back then often find their slot recycled and take the L2
-// path).
-constexpr int kTileRing = 2048;  // ring slots (64 KB of shared memory)
-
-template <int LG, int BS, bool UP, int RING>
-static void launch_tile_r(const TileSched& t, const double* vals, const double* invd, const double* b, double* x,
-                          double* reset, const int* done, cudaStream_t st) {
-    constexpr size_t smem = sizeof(TileSlot) * RING;
-    static bool set = false;
-    if (!set) {
-        CK(cudaFuncSetAttribute(tile_trsv_kernel<LG, BS, UP, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-        set = true;
-    }
-    tile_trsv_kernel<LG, BS, UP, RING><<<t.ntiles, 512, smem, st>>>(t.tbeg.p, t.srp.p, t.tcol.p, vals,
-                                                                     invd, b, x, reset, done);
-}
-
-template <int LG, int BS, bool UP>
-static void launch_tile_t(const Schedule& s, const double* vals, const double* invd, const double* b, double* x,
-                          double* reset, const int* done, cudaStream_t st) {
-    static const bool small = getenv("PCLAB_TILE_RING") && atoi(getenv("PCLAB_TILE_RING")) == 64;
-    if (small) launch_tile_r<LG, BS, UP, 64>(s.tile, vals, invd, b, x, reset, done, st);
-    else launch_tile_r<LG, BS, UP, kTileRing>(s.tile, vals, invd, b, x, reset, done, st);
+    const unsigned grid = std::min(trsv_grid(s, 6.0, RR_THREADS / 32), cap);
+    rr_trsv_kernel<LG, BS, UP, CH><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.slot_rp.p, M.cols.p, vals, invd, b, x,
+                                                                reset, done);
 }
 
 template <int BS, bool UP>
 static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const BlockCols* bc, const double* vals,
                            const double* invd, const double* b, double* x, double* reset, const int* done,
-                           unsigned* ctr, cudaStream_t st, bool pad, const RUpdate* ru) {
-    if ((pad || ru) && !bc) throw DimensionError("padded / fused-residual sweeps need the node-blocked sweep");
+                           unsigned* ctr, cudaStream_t st, bool pad) {
+    if (pad && !bc) throw DimensionError("padded sweeps need the node-blocked sweep");
     if constexpr (BS > 1) {
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
-            if (s.tile.ntiles > 0 && !pad && !ru) {
-                switch (s.lanes) {
-                    case 2:
-                    case 4: launch_tile_t<4, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
-                    case 8: launch_tile_t<8, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
-                    case 16: launch_tile_t<16, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
-                    default: launch_tile_t<32, BS, UP>(s, vals, invd, b, x, reset, done, st); break;
-                }
-                return;
-            }
-            bool chained = false;
-            if (!pad) chained = launch_chain_t<BS, UP>(s, *bc, M, vals, invd, b, x, reset, done, st);
-            if (chained) return;
             switch (s.lanes) {
             case 2:
-            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
-            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
-            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
-            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad, ru); break;
+            case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
+            default: launch_bsr_t<32, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
             }
             return;
         }
@@ -468,45 +340,20 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
 
 // Launch one sweep; `ctr` must be zero on entry. Caller owns x (filled
 // with kPending) and the optional reset buffer.
-void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x, double* reset, const int* done, unsigned* ctr,
-                 cudaStream_t st, bool pad, const RUpdate* ru) {
+void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
+                 double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const DevCsr& M = upper ? an.upper : an.lower;
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
     if (upper) {
-        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
-        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
-        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
+        if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else launch_trsv_bs<1, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
     } else {
-        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
-        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
-        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad, ru);
-    }
-    CK_LAUNCH();
-}
-
-// ctr[0..2] must be zero on entry (sweep items, CTA roles, product pairs).
-void launch_trsv_fused(const Analysis& an, const DevCsr& A, const double* uvals, const double* invd,
-                       const double* y, double* z, double* reset, double* w, const int* done, unsigned* ctr,
-                       cudaStream_t st) {
-    if (an.blk_up.nitems == 0) return;
-    if (an.bs == 3) {
-        switch (an.blk_up.lanes) {
-            case 2:
-            case 4: launch_fused_t<4, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            case 8: launch_fused_t<8, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            case 16: launch_fused_t<16, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            default: launch_fused_t<32, 3>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-        }
-    } else {
-        switch (an.blk_up.lanes) {
-            case 2:
-            case 4: launch_fused_t<4, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            case 8: launch_fused_t<8, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            case 16: launch_fused_t<16, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-            default: launch_fused_t<32, 2>(an, A, uvals, invd, y, z, reset, w, done, ctr, st); break;
-        }
+        if (an.bs == 3) launch_trsv_bs<3, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else if (an.bs == 2) launch_trsv_bs<2, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
+        else launch_trsv_bs<1, false>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
     }
     CK_LAUNCH();
 }
@@ -516,23 +363,10 @@ void trsv(const Analysis& an, const double* vals, const double* invd, bool upper
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
     fill_pending(x, an.lower.n, st);
-    // the caller's right-hand side into a library buffer (aligned, padded:
-    // the chain sweep streams it with bulk copies)
-    DevBuf<double> bcopy(an.lower.n);
-    if (an.lower.n) CK(cudaMemcpyAsync(bcopy.p, b, sizeof(double) * an.lower.n, cudaMemcpyDeviceToDevice, st));
-    b = bcopy.p;
-    const char* tf = getenv("PCLAB_TRSV_TRACE");
-    const Schedule& s = upper ? an.blk_up : an.blk_lo;
-    DevBuf<long long> tb;
-    if (tf) {
-        tb.alloc(4 * (s.nitems * s.per_item + s.nblocks));
-        g_trace = tb.p;
-    }
     // 3x3 node-blocked sweeps run on the padded layout of the PCG loop
     // (4 doubles per node: 256-bit polls / publications): the right-hand
     // side of the backward sweep and the output go through padded copies
-    static const bool padz_env = !(getenv("PCLAB_PADZ") && atoi(getenv("PCLAB_PADZ")) == 0);
-    const bool pad = padz_env && an.bsr && an.bs == 3 && !tf && s.tile.ntiles == 0;
+    const bool pad = an.bsr && an.bs == 3;
     if (pad) {
         const int64_t n = an.lower.n, n4 = 4 * (n / 3);
         DevBuf<double> x4(n4), b4;
@@ -551,35 +385,6 @@ void trsv(const Analysis& an, const double* vals, const double* invd, bool upper
     }
     launch_trsv(an, vals, invd, upper, b, x, nullptr, nullptr, ctr.p, st);
     CK(cudaStreamSynchronize(st));
-    g_trace = nullptr;
-    if (tf) {
-        std::vector<long long> h(tb.n);
-        CK(cudaMemcpy(h.data(), tb.p, tb.bytes(), cudaMemcpyDeviceToHost));
-        std::string path = std::string(tf) + (upper ? ".up" : ".lo");
-        FILE* f = fopen(path.c_str(), "wb");
-        if (f) {
-            fwrite(h.data(), sizeof(long long), h.size(), f);
-            fclose(f);
-        }
-        // levels of the items (block level of the first slot)
-        std::vector<int32_t> lv(s.nblocks), sl(s.nitems * s.per_item);
-        CK(cudaMemcpy(lv.data(), s.level.p, sizeof(int32_t) * s.nblocks, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(sl.data(), s.slots.p, sizeof(int32_t) * sl.size(), cudaMemcpyDeviceToHost));
-        std::vector<int32_t> il(s.nitems);
-        for (int64_t i = 0; i < s.nitems; ++i) il[i] = lv[sl[i * s.per_item]];
-        std::vector<int32_t> cr(s.nblocks);
-        CK(cudaMemcpy(cr.data(), s.crit.p, sizeof(int32_t) * s.nblocks, cudaMemcpyDeviceToHost));
-        auto dump = [&](const std::string& p, const std::vector<int32_t>& v) {
-            FILE* g = fopen(p.c_str(), "wb");
-            if (g) {
-                fwrite(v.data(), sizeof(int32_t), v.size(), g);
-                fclose(g);
-            }
-        };
-        dump(path + ".lev", il);
-        dump(path + ".slots", sl);
-        dump(path + ".crit", cr);
-    }
 }
 
 __global__ void invd_kernel(int64_t n, const int64_t* __restrict__ lrp, const double* __restrict__ l,

@@ -31,13 +31,9 @@ constexpr int kT = 256;
 struct Scal {
     double rz, pap, alpha, beta, bnorm, rel, rel_tol, rr;
     long long iter, max_iters;
-    // done_sweep: the done flag as of the product, read by the sweeps of the
-    // fused-residual loop -- the concurrent x / ||r|| kernel may raise `done`
-    // while a sweep's CTAs are starting, and a sweep whose CTAs disagree on it
-    // would leave items unprocessed
-    int done, converged, error, done_sweep;
+    int done, converged, error, pad;
     unsigned ticket[4];
-    unsigned ctr[4];  // sweep L items, sweep U items, fused CTA roles, product pairs
+    unsigned ctr[4];  // claim counters of the fallback sweeps (L, U)
 };
 
 // Last-CTA finalisation of a per-CTA partial: returns true in the CTA
@@ -205,10 +201,7 @@ __global__ void __launch_bounds__(kT, PAP4_MINB)
 k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __restrict__ bp,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals, const double* __restrict__ p4,
                 double* __restrict__ q, Scal* S, double* part) {
-    if (S->done) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) S->done_sweep = 1;
-        return;
-    }
+    if (S->done) return;
     constexpr int BS = 3;
     const int lane = threadIdx.x & 31;
     const int gw = static_cast<int>((blockIdx.x * kT + threadIdx.x) >> 5);
@@ -271,7 +264,6 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
         } else {
             S->alpha = S->rz / tot;
         }
-        S->done_sweep = S->done;
         S->ctr[0] = 0;
         S->ctr[1] = 0;
         S->ctr[2] = 0;
@@ -283,46 +275,6 @@ k_spmv_bsr_pap4(int64_t nb, const int64_t* __restrict__ rp, const int64_t* __res
 __global__ void __launch_bounds__(kT)
 k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
         double* __restrict__ r, Scal* S, double* part, double* hist);
-
-// x += alpha p (padded p) and ||r - alpha q|| -> convergence, r not written:
-// runs concurrently with the forward sweep that forms and stores r_new
-// itself (RUpdate); own partials buffer (the dot may overlap it)
-__global__ void __launch_bounds__(kT)
-k_xrr4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
-       const double* __restrict__ r, Scal* S, double* part, double* hist);
-
-// Fused-product variant (Analysis::fused_up): w = A z came out of the
-// backward sweep, so p <- z + beta p, q <- w + beta q (= A p by linearity)
-// and pq in one vector pass; alpha = rz / pq.
-__global__ void __launch_bounds__(kT)
-k_pq(int64_t n, const double* __restrict__ z, const double* __restrict__ w, double* __restrict__ p,
-     double* __restrict__ q, Scal* S, double* part) {
-    if (S->done) return;
-    const double beta = S->beta;
-    double loc = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * kT) {
-        const double pi = fma(beta, p[i], z[i]);
-        const double qi = fma(beta, q[i], w[i]);
-        p[i] = pi;
-        q[i] = qi;
-        loc = fma(pi, qi, loc);
-    }
-    double tot;
-    if (finish_partial(loc, part, &S->ticket[0], &tot) && threadIdx.x == 0) {
-        S->pap = tot;
-        if (!(tot > 0.0)) {
-            S->error = 1;
-            S->done = 1;
-        } else {
-            S->alpha = S->rz / tot;
-        }
-        S->ctr[0] = 0;
-        S->ctr[1] = 0;
-        S->ctr[2] = 0;
-        S->ctr[3] = 0;
-    }
-}
 
 // q = A p and pAp for a node-blocked A (Analysis::a_bsr): warp per block
 // row (grid-stride), the next row's pointers loaded while this one runs.
@@ -408,35 +360,6 @@ k_axpy4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, 
         x[i] = fma(alpha, p4[p4_index(i)], x[i]);
         const double ri = fma(-alpha, q[i], r[i]);
         r[i] = ri;
-        loc = fma(ri, ri, loc);
-    }
-    double tot;
-    if (finish_partial(loc, part, &S->ticket[1], &tot) && threadIdx.x == 0) {
-        S->rr = tot;
-        const double rel = sqrt(tot) / S->bnorm;
-        const long long it = S->iter + 1;
-        S->iter = it;
-        S->rel = rel;
-        if (hist) hist[it] = rel;
-        if (rel <= S->rel_tol) {
-            S->converged = 1;
-            S->done = 1;
-        } else if (it >= S->max_iters) {
-            S->done = 1;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kT)
-k_xrr4(int64_t n, const double* __restrict__ p4, const double* __restrict__ q, double* __restrict__ x,
-       const double* __restrict__ r, Scal* S, double* part, double* hist) {
-    if (S->done) return;
-    const double alpha = S->alpha;
-    double loc = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * kT) {
-        x[i] = fma(alpha, p4[p4_index(i)], x[i]);
-        const double ri = fma(-alpha, q[i], r[i]);
         loc = fma(ri, ri, loc);
     }
     double tot;
@@ -671,7 +594,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     CK(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     const int parts_max = sm_count() * 8;
     DevBuf<Scal> S(1);
-    DevBuf<double> part(parts_max), r(n), q(n), pa, y, zbuf, wbuf, tmp(n);
+    DevBuf<double> part(parts_max), r(n), q(n), pa, y, zbuf, tmp(n);
     DevBuf<double> hist;
     if (record) hist.alloc(max_iters + 1);
     Scal h{};
@@ -679,8 +602,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     h.max_iters = max_iters;
     CK(cudaMemcpyAsync(S.p, &h, sizeof h, cudaMemcpyHostToDevice, st));
     // vector kernels: 8 CTAs per SM (axpy 58 -> 45 us, dot 26 -> 25 us on configs[2])
-    static const int vmul = std::min(getenv("PCLAB_VGRID") ? atoi(getenv("PCLAB_VGRID")) : 8, 8);
-    const unsigned vgrid = static_cast<unsigned>(sm_count() * vmul);
+    const unsigned vgrid = static_cast<unsigned>(sm_count() * 8);
     const unsigned sgrid = static_cast<unsigned>(sm_count() * 8);
     if (n) k_dot<<<vgrid, kT, 0, st>>>(n, b, b, S.p, part.p, 2);
     CK_LAUNCH();
@@ -710,19 +632,14 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     }
     trace("setup");
     const Analysis* an = factor ? a.an.get() : nullptr;
-    // backward sweep fused with the product (node-blocked matrices)
-    const bool fused = an && an->fused_up;
-    // padded p for the node-blocked 3x3 product (PCLAB_PADP=0: plain p)
-    static const bool padp_env = !(getenv("PCLAB_PADP") && atoi(getenv("PCLAB_PADP")) == 0);
+    if (factor && !an) throw DimensionError("pcg: the preconditioner's matrix analysis was dropped");
+    // padded p for the node-blocked 3x3 product
     // (k_spmv_bsr_pap4 indexes A's entries and block columns with 32 bits)
-    const bool padp = padp_env && an && an->a_bsr && an->bs == 3 && !fused && a.a.nnz < (1LL << 32) &&
-                      an->abc.bcol.n < (1LL << 32);
+    const bool padp = an && an->a_bsr && an->bs == 3 && a.a.nnz < (1LL << 32) && an->abc.bcol.n < (1LL << 32);
     pa.alloc(padp ? 4 * (n / 3) : n);
     // sweep vectors y, z padded too (node-blocked 3x3 sweeps): 256-bit polls
-    // and publications (bsr_item PAD); PCLAB_PADZ=0 keeps them plain
-    static const bool padz_env = !(getenv("PCLAB_PADZ") && atoi(getenv("PCLAB_PADZ")) == 0);
-    const bool padz = padz_env && padp && an->bsr && an->bs == 3;
-    if (fused) wbuf.alloc(n);
+    // and publications (bsr_item PAD)
+    const bool padz = padp && an->bsr && an->bs == 3;
     double* z = r.p;  // kind none: z aliases r
     if (factor) {
         y.alloc(padz ? 4 * (n / 3) : n);
@@ -740,10 +657,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
             launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st, padz);
-            if (fused)
-                launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, nullptr, S.p->ctr + 1, st);
-            else
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
+            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
@@ -755,9 +669,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     else
         k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 1);
     CK(cudaMemsetAsync(pa.p, 0, pa.bytes(), st));
-    CK(cudaMemsetAsync(q.p, 0, sizeof(double) * n, st));  // fused: q <- w + 0 q
     CK_LAUNCH();
-    // ---- capture an even number of iterations (p buffers alternate)
     const int lpr = spmv_lanes(a);
     static const unsigned tgrid = [] {
         int per_sm = 0;
@@ -772,55 +684,10 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
     static const unsigned bsr_grid3 = one_wave(k_spmv_bsr_pap<3>);
     static const unsigned bsr_grid2 = one_wave(k_spmv_bsr_pap<2>);
     static const unsigned bsr_grid4 = one_wave(k_spmv_bsr_pap4);
-    // forward sweep fused with the residual update, x / ||r|| on a side
-    // stream (padded node-blocked loop). Opt-in (PCLAB_RAX=1): on configs[2]
-    // the loop gains ~9 us per iteration (k_axpy4 hidden, the forward sweep
-    // 25 us slower with the extra q load / r store) -- within run-to-run noise
-    static const bool rax_env = getenv("PCLAB_RAX") && atoi(getenv("PCLAB_RAX")) != 0;
-    const bool rax = rax_env && padz;
-    DevBuf<double> r2, part2;
-    if (rax) {
-        r2.alloc(n);
-        part2.alloc(parts_max);
-    }
-    int rpar = 0;            // residual buffer parity (r, r2 alternate)
-    bool seq_side = false;   // profiling: the side kernel runs in order
-    bool side_pending = false;
-    static thread_local cudaStream_t side = [] {
-        cudaStream_t t;
-        CK(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
-        return t;
-    }();
-    cudaEvent_t ev_fork, ev_join;
-    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    auto join_side = [&] {
-        if (side_pending) {
-            CK(cudaStreamWaitEvent(st, ev_join, 0));
-            side_pending = false;
-        }
-    };
-    // `mark` runs after each of the five kernels (event hook for profiling)
-    auto iteration_parts = [&](double* pp, double* /*unused*/, auto&& mark) {
-        if (fused) {
-            // [p, q, alpha] -> [x, r] -> y = L^-1 r -> [z = U^-1 y, w = A z] -> beta
-            k_pq<<<vgrid, kT, 0, st>>>(n, z, wbuf.p, pp, q.p, S.p, part.p);
-            mark();
-            k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
-            mark();
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
-            mark();
-            launch_trsv_fused(*an, a.a, pc.uvals.p, pc.invd.p, y.p, z, y.p, wbuf.p, &S.p->done, S.p->ctr + 1, st);
-            mark();
-            k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
-            mark();
-            return;
-        }
+    // one PCG iteration, five or six kernels; `mark` runs after each stage
+    // (event hook for profiling): [product, axpy, sweep L, sweep U, dot]
+    auto iteration_parts = [&](double* pp, auto&& mark) {
         if (padp) {
-            if (side_pending) {  // the previous iteration's x update read p
-                CK(cudaStreamWaitEvent(st, ev_join, 0));
-                side_pending = false;
-            }
             if (padz)
                 k_pupdate4<true><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
             else
@@ -829,91 +696,53 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             k_spmv_bsr_pap4<<<bsr_grid4, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p, S.p,
                                                      part.p);
             mark();
-            if (rax) {
-                // r_new = r - alpha q is formed by the forward sweep itself; x
-                // and ||r_new|| on a side stream, concurrent with the sweeps
-                // (joined before the next p update, which overwrites p)
-                double* rold = rpar ? r2.p : r.p;
-                double* rnew = rpar ? r.p : r2.p;
-                rpar ^= 1;
-                if (seq_side) {
-                    k_xrr4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, rold, S.p, part2.p, record ? hist.p : nullptr);
-                } else {
-                    CK(cudaEventRecord(ev_fork, st));
-                    CK(cudaStreamWaitEvent(side, ev_fork, 0));
-                    k_xrr4<<<vgrid, kT, 0, side>>>(n, pp, q.p, x, rold, S.p, part2.p, record ? hist.p : nullptr);
-                    CK(cudaEventRecord(ev_join, side));
-                    side_pending = true;
-                }
-                mark();
-                RUpdate ru;
-                ru.q = q.p;
-                ru.rnew = rnew;
-                ru.alpha = &S.p->alpha;
-                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, rold, y.p, z, &S.p->done_sweep, S.p->ctr, st, true,
-                            &ru);
-                mark();
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done_sweep, S.p->ctr + 1, st, true);
-                mark();
-                k_dot_z4<<<vgrid, kT, 0, st>>>(n, rnew, z, S.p, part.p, 0);
-                mark();
-                return;
-            }
             k_axpy4<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
             mark();
-            if (factor) {
-                launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st, padz);
-                mark();
-                launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st, padz);
-                mark();
+        } else {
+            k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
+            if (an && an->a_bsr) {
+                // grid = one resident wave (grid-stride rows; a second partial
+                // wave doubles the tail: measured 0.75 vs 0.93 ms at 1.5 waves)
+                const BlockCols& bc = an->abc;
+                if (an->bs == 3)
+                    k_spmv_bsr_pap<3><<<bsr_grid3, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp,
+                                                               q.p, S.p, part.p);
+                else
+                    k_spmv_bsr_pap<2><<<bsr_grid2, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp,
+                                                               q.p, S.p, part.p);
+            } else switch (lpr) {
+                case 1: k_spmv_tile_pap<<<tgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 9: k_spmv_pap<8, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 5: k_spmv_pap<4, 8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 3: k_spmv_pap<4, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 2: k_spmv_pap<2, 16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 17: k_spmv_pap<16, 3><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                case 16: k_spmv_pap<16, 6><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
+                default: k_spmv_pap<32, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
             }
-            if (padz)
-                k_dot_z4<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
-            else
-                k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
             mark();
-            return;
+            k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
+            mark();
         }
-        k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
-        if (an && an->a_bsr) {
-            // grid = one resident wave (grid-stride rows; a second partial
-            // wave doubles the tail: measured 0.75 vs 0.93 ms at 1.5 waves)
-            const BlockCols& bc = an->abc;
-            if (an->bs == 3)
-                k_spmv_bsr_pap<3><<<bsr_grid3, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
-                                                           S.p, part.p);
-            else
-                k_spmv_bsr_pap<2><<<bsr_grid2, kT, 0, st>>>(n / 2, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p,
-                                                           S.p, part.p);
-        } else switch (lpr) {
-            case 1: k_spmv_tile_pap<<<tgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 4: k_spmv_pap<4, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 8: k_spmv_pap<8, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 9: k_spmv_pap<8, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 5: k_spmv_pap<4, 8><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 3: k_spmv_pap<4, 12><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 2: k_spmv_pap<2, 16><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 17: k_spmv_pap<16, 3><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            case 16: k_spmv_pap<16, 6><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-            default: k_spmv_pap<32, 4><<<sgrid, kT, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.a.vals.p, pp, q.p, S.p, part.p); break;
-        }
-        mark();
-        k_axpy<<<vgrid, kT, 0, st>>>(n, pp, q.p, x, r.p, S.p, part.p, record ? hist.p : nullptr);
-        mark();
         if (factor) {
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st);
+            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st, padz);
             mark();
-            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st);
+            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st, padz);
             mark();
         } else {
             if (pc.kind == Kind::Jacobi) k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
             mark();
             mark();
         }
-        k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+        if (padz)
+            k_dot_z4<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
+        else
+            k_dot<<<vgrid, kT, 0, st>>>(n, r.p, z, S.p, part.p, 0);
         mark();
     };
-    auto iteration = [&](double* pold, double* pnew) { iteration_parts(pold, pnew, [] {}); };
+    auto iteration = [&](double* pp) { iteration_parts(pp, [] {}); };
     // pinned done flag, allocated once per host thread: a pinned allocation
     // inside the timed solve could stall the host (page pinning) while the
     // GPU idles
@@ -923,21 +752,17 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         return h;
     }();
     if (prof_ms) {
-        seq_side = true;  // the side kernel in stream order: its own slot
         // eager iterations with an event between kernels: per-kernel device
-        // times averaged over iterations, [spmv_p, axpy, sweep L, sweep U,
-        // dot] or, fused, [pq, axpy, sweep L, sweep U + A z, dot]
+        // times averaged over iterations, [spmv_p, axpy, sweep L, sweep U, dot]
         constexpr int kK = 5;
         cudaEvent_t ev[kK + 1];
         for (auto& e : ev) CK(cudaEventCreate(&e));
         double acc[kK] = {0, 0, 0, 0, 0};
         int done_iters = 0;
-        double* pold = pa.p;
-        double* pnew = nullptr;
         for (;;) {
             int k = 0;
             CK(cudaEventRecord(ev[k++], st));
-            iteration_parts(pold, pnew, [&] { CK(cudaEventRecord(ev[k++], st)); });
+            iteration_parts(pa.p, [&] { CK(cudaEventRecord(ev[k++], st)); });
             CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             if (*hdone) break;  // converged inside: the partial iteration is not counted
@@ -950,30 +775,18 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         }
         for (int t = 0; t < kK; ++t) prof_ms[t] = done_iters ? acc[t] / done_iters : 0.0;
         prof_ms[kK] = done_iters;
-        prof_ms[kK + 1] = fused ? 1.0 : 0.0;
+        prof_ms[kK + 1] = 0.0;
         prof_ms[kK + 2] = 0.0;
         for (auto& e : ev) cudaEventDestroy(e);
-    } else if (getenv("PCLAB_PCG_GRAPH") && atoi(getenv("PCLAB_PCG_GRAPH")) == 0) {
-        // developer knob: stream-launched iterations, done flag read every 8
-        for (;;) {
-            for (int k = 0; k < 8; ++k) iteration(pa.p, nullptr);
-            join_side();
-            CK(cudaMemcpyAsync(hdone, &S.p->done, sizeof(int), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (*hdone) break;
-        }
     } else {
-        static const int pairs_env = getenv("PCLAB_GRAPH_PAIRS") ? atoi(getenv("PCLAB_GRAPH_PAIRS")) : 0;
-        const int pairs = pairs_env > 0 ? pairs_env : (n > 2000000 ? 4 : 8);  // iterations per graph = 2 * pairs
+        // iterations captured in a CUDA graph; the host reads the done flag
+        // once per replay (every kernel no-ops after convergence)
+        const int per_graph = n > 2000000 ? 8 : 16;
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         const long long before = launch_count();
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        for (int k = 0; k < pairs; ++k) {
-            iteration(pa.p, nullptr);
-            iteration(pa.p, nullptr);
-        }
-        join_side();  // the side stream rejoins before the capture ends
+        for (int k = 0; k < per_graph; ++k) iteration(pa.p);
         CK(cudaStreamEndCapture(st, &graph));
         trace("captured");
         CK(cudaGraphInstantiate(&exec, graph, 0));
@@ -995,9 +808,6 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         cudaGraphExecDestroy(exec);
         cudaGraphDestroy(graph);
     }
-    join_side();
-    cudaEventDestroy(ev_fork);
-    cudaEventDestroy(ev_join);
     trace("loop done");
     rep.cg_time = cg.ms() / 1e3;
     CK(cudaMemcpyAsync(&h, S.p, sizeof h, cudaMemcpyDeviceToHost, st));

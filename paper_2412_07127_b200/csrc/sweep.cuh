@@ -8,32 +8,16 @@
 #ifndef TRSV_MINB
 #define TRSV_MINB 4
 #endif
-// the node-blocked sweep runs ~2 levels of items (<= 2 CTAs per SM): give
-// it the registers to keep the two items' operands without spilling
-#ifndef BSR_MINB
-#define BSR_MINB 2
-#endif
 // node-blocked sweep CTA: 128 threads, 7 resident per SM (28 warps at <= 72
-// registers; a few bytes of spill), entries prefetched into L1 one item
-// ahead (slot records two ahead). Measured on configs[2], production build
-// (no developer probes), per sweep: 6/SM 0.868 ms, 7/SM 0.859, 7/SM with
-// one-item prefetch 0.849, 8/SM 1.02 (spills)
+// registers), entries prefetched into L1 one item ahead (slot records two
+// ahead). Measured on configs[2] per sweep: 6/SM 0.868 ms, 7/SM 0.859, 7/SM
+// with one-item prefetch 0.849, 8/SM 1.02 (spills)
 #ifndef BSR_THREADS
 #define BSR_THREADS 128
 #endif
 #ifndef BSR_CTAS
 #define BSR_CTAS 7
 #endif
-#ifndef BSR_PF
-#define BSR_PF 1
-#endif
-// 1: right-hand side loaded an item ahead into registers; 0: at item start
-// (its latency hides behind the dependency polls; 6 registers fewer, no
-// spills at 7 CTAs/SM: 0.836 -> 0.823 ms)
-#ifndef BSR_RHS_AHEAD
-#define BSR_RHS_AHEAD 0
-#endif
-
 
 namespace pclab_b200 {
 
@@ -177,6 +161,37 @@ __device__ __forceinline__ void bsr_row_dot(const BsrRow<BS>& m, const int32_t* 
     for (int t = 0; t < BS; ++t) acc[t] = group_sum<32>(acc[t]);
 }
 
+// Dense BSxBS diagonal block of a sweep item: rows forward (L, in-block
+// entries left of the diagonal in `bin`, row by row) or backward (U, right
+// of the diagonal), each row s = rhs - acc - sum(bin * x), x = s / l_tt as
+// s * (1 / l_tt).
+template <int BS, bool UPPER>
+__device__ __forceinline__ void solve_diag_block(const double (&rhs)[BS], const double (&acc)[BS],
+                                                 const double* bin, const double (&binv)[BS], double (&xb)[BS]) {
+    if (!UPPER) {
+        int q = 0;
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            double s = rhs[t] - acc[t];
+#pragma unroll
+            for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
+            xb[t] = s * binv[t];
+        }
+    } else {
+#pragma unroll
+        for (int t = BS - 1; t >= 0; --t) {
+            double s = rhs[t] - acc[t];
+            // bin holds, row by row, U[t][s] for s > t
+            int q = 0;
+#pragma unroll
+            for (int r = 0; r < t; ++r) q += BS - 1 - r;
+#pragma unroll
+            for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
+            xb[t] = s * binv[t];
+        }
+    }
+}
+
 // Per-item state of a sweep, loaded one item ahead.
 template <int BS>
 struct SweepMeta {
@@ -233,11 +248,8 @@ __global__ void __launch_bounds__(256, TRSV_MINB)
 trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __restrict__ crit,
             const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
             const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs,
-            double* out, double* reset, const int* __restrict__ done, unsigned* counter,
-            int tune, long long* trace) {
+            double* out, double* reset, const int* __restrict__ done, unsigned* counter) {
     if (done && *done) return;
-    const bool use_crit = (tune & 0xff) == 0;
-    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
     constexpr int G = 32 / LG;
     // entries per lane per round: one round covers a 3x3-blocked elasticity
     // node (<= 117 off-block entries) so every load is issued before any spin
@@ -268,8 +280,6 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
         }
         unsigned after = 0;
         if (lane == 0) after = atomicAdd(counter, 1u);
-        long long tr0 = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         const bool active = m.blk >= 0;
         const int64_t r0 = active ? m.blk * BS : 0;
         int64_t ob[BS], oc[BS];
@@ -327,19 +337,15 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
         // park the waiting half of the warp for microseconds); the group's
         // lanes poll the same address, so it is one request per group
         {
-            const bool poll = use_crit && active && m.crit >= 0;
+            const bool poll = active && m.crit >= 0;
             while (__any_sync(0xffffffffu, poll && is_pending(ld_relaxed(out + (poll ? m.crit : 0))))) {
-                if (sleep_ns) __nanosleep(sleep_ns);
             }
         }
-        long long tr1 = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
         // (3) gather the dependencies
         double acc[BS];
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = 0.0;
         const int tmax = __reduce_max_sync(0xffffffffu, total);
-        int rounds = 0;
         for (int base = 0; base < tmax; base += LG * CH) {
             if (base > 0) load_chunk(base);
             double xv[CH];
@@ -349,8 +355,6 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
 #pragma unroll
             for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
             while (__any_sync(0xffffffffu, pend)) {
-                ++rounds;
-                if (sleep_ns) __nanosleep(sleep_ns);
                 pend = false;
 #pragma unroll
                 for (int c = 0; c < CH; ++c)
@@ -365,49 +369,15 @@ trsv_kernel(int64_t nitems, const int32_t* __restrict__ slots, const int32_t* __
                 for (int t = 0; t < BS; ++t)
                     if (tt[c] == t) acc[t] = fma(v[c], xv[c], acc[t]);
         }
-        long long trg = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
         after = __shfl_sync(0xffffffffu, after, 0);
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
         // (4) diagonal block
         if (active && gl == 0) {
             double xb[BS];
-            if (!UPPER) {
-                int q = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    double s = brhs[t] - acc[t];
-#pragma unroll
-                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            } else {
-#pragma unroll
-                for (int t = BS - 1; t >= 0; --t) {
-                    double s = brhs[t] - acc[t];
-                    // bin holds, row by row, U[t][s] for s > t
-                    int q = 0;
-#pragma unroll
-                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            }
+            solve_diag_block<BS, UPPER>(brhs, acc, bin, binv, xb);
 #pragma unroll
             for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
-        }
-        if (trace && lane == 0) {
-            long long tr2;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            trace[4LL * it + 0] = tr0;
-            trace[4LL * it + 1] = tr1;
-            trace[4LL * it + 2] = tr2;
-            (void)smid;
-            trace[4LL * it + 3] = (trg - tr1) * 1024 + min(rounds, 1023);  // gather ns | re-poll rounds
         }
         __syncwarp();
         if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
@@ -477,21 +447,10 @@ __device__ __forceinline__ int slot_nb(const BsrSlot& m) {
 // and every load is issued a whole item before its value is needed:
 //   item k+3: slot record        item k+2: entries prefetched into L1
 //   item k+1: right-hand side    item k:   entries, dependency polls
-// Forward sweep fused with the residual update (PCG loop, RAX): the
-// right-hand side of block b is r_new = r - alpha q, computed as it is
-// loaded (the fma k_axpy uses) and written to `rnew` by the group's lane 0;
-// x and ||r_new|| are updated by a concurrent kernel.
-struct RUpdate {
-    const double* q = nullptr;
-    double* rnew = nullptr;
-    const double* alpha = nullptr;
-};
-
 // One item of the node-blocked sweep: this lane group's block `m` (rows
 // r0..r0+BS-1, right-hand side rc), lane gl owning neighbour blocks gl,
 // gl+LG, ...: stream the 3x3 values, poll the neighbours' values, reduce,
-// solve the diagonal block, publish, re-arm `reset`. `flags` = experiment
-// bits of the tune word (see bsr_sweep).
+// solve the diagonal block, publish, re-arm `reset`.
 //
 // PAD (BS = 3, inside the PCG loop): the sweep's output / re-arm vectors are
 // stored padded, 4 doubles per node, so a dependency poll is ONE 256-bit
@@ -511,14 +470,12 @@ __device__ __forceinline__ void st_relaxed_v4(double* p, double a, double b, dou
                  : "memory");
 }
 
-template <int LG, int BS, bool UPPER, bool PAD = false, bool RAX = false>
+template <int LG, int BS, bool UPPER, bool PAD = false>
 __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS], const int32_t* __restrict__ bcol,
                                          const double* __restrict__ vals, const double* __restrict__ invd,
-                                         double* out, double* reset, unsigned sleep_ns, int flags, int64_t it,
-                                         long long* trace, long long tr0, double* rnew = nullptr) {
+                                         double* out, double* reset) {
     static_assert(!PAD || BS == 3, "padded vectors hold 3-dof nodes");
     constexpr int NIB = BS * (BS - 1) / 2;
-    const bool exp_vals = flags & 1, exp_nowait = flags & 2, exp_nox = flags & 4;
     const int lane = threadIdx.x & 31;
     const int gl = lane % LG;
     const bool active = m.blk >= 0;
@@ -551,7 +508,6 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
 #pragma unroll
     for (int t = 0; t < BS; ++t) acc[t] = 0.0;
     const int nbmax = __reduce_max_sync(0xffffffffu, nb);
-    int rounds = 0;
     // RU neighbour rounds per pass with every load of the pass issued
     // before the first poll (LG = 8: a lane owns neighbours gl and gl + 8)
     constexpr int RU = LG <= 8 ? 2 : 1;
@@ -569,8 +525,7 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
 #pragma unroll
                 for (int t = 0; t < BS; ++t)
 #pragma unroll
-                    for (int c = 0; c < BS; ++c)
-                        a[r][t][c] = ld_stream(vals + (exp_vals ? t * BS + c : ob[t] + BS * n + c));
+                    for (int c = 0; c < BS; ++c) a[r][t][c] = ld_stream(vals + ob[t] + BS * n + c);
             } else {
 #pragma unroll
                 for (int t = 0; t < BS; ++t)
@@ -582,22 +537,14 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
         for (int r = 0; r < RU; ++r) {
             if (own[r]) {
                 if constexpr (PAD) {
-                    if (exp_nox) {
+                    double w3[3];
+                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc[r] / 3), w3);
 #pragma unroll
-                        for (int c = 0; c < BS; ++c) xv[r][c] = 1.0;
-                    } else {
-                        double w3[3];
-                        ld_relaxed_v4(out + 4 * static_cast<int64_t>(xc[r] / 3), w3);
-#pragma unroll
-                        for (int c = 0; c < BS; ++c) xv[r][c] = w3[c];
-                    }
+                    for (int c = 0; c < BS; ++c) xv[r][c] = w3[c];
                 } else {
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[r][c] = exp_nox ? 1.0 : ld_relaxed(out + xc[r] + c);
+                    for (int c = 0; c < BS; ++c) xv[r][c] = ld_relaxed(out + xc[r] + c);
                 }
-                if (exp_nowait)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[r][c] = is_pending(xv[r][c]) ? 0.0 : xv[r][c];
             } else {
 #pragma unroll
                 for (int c = 0; c < BS; ++c) xv[r][c] = 0.0;
@@ -609,8 +556,6 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
 #pragma unroll
             for (int c = 0; c < BS; ++c) pend |= own[r] && is_pending(xv[r][c]);
         while (__any_sync(0xffffffffu, pend)) {
-            ++rounds;
-            if (sleep_ns) __nanosleep(sleep_ns);
             pend = false;
 #pragma unroll
             for (int r = 0; r < RU; ++r) {
@@ -644,37 +589,11 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
 #pragma unroll
                 for (int c = 0; c < BS; ++c) acc[t] = fma(a[r][t][c], xv[r][c], acc[t]);
     }
-    long long trg = 0;
-    if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg));
 #pragma unroll
     for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
     if (active && gl == 0) {
         double xb[BS];
-        if (!UPPER) {
-            int q = 0;
-#pragma unroll
-            for (int t = 0; t < BS; ++t) {
-                double s = rc[t] - acc[t];
-#pragma unroll
-                for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                xb[t] = s * binv[t];
-            }
-        } else {
-#pragma unroll
-            for (int t = BS - 1; t >= 0; --t) {
-                double s = rc[t] - acc[t];
-                int q = 0;
-#pragma unroll
-                for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                xb[t] = s * binv[t];
-            }
-        }
-        if constexpr (RAX) {
-#pragma unroll
-            for (int t = 0; t < BS; ++t) rnew[r0 + t] = rc[t];
-        }
+        solve_diag_block<BS, UPPER>(rc, acc, bin, binv, xb);
         if constexpr (PAD) {
             st_relaxed_v4(out + 4 * static_cast<int64_t>(m.blk), xb[0], xb[1], xb[2], 0.0);
         } else {
@@ -682,32 +601,17 @@ __device__ __forceinline__ void bsr_item(const BsrSlot& m, const double (&rc)[BS
             for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
         }
     }
-    if (trace && lane == 0) {
-        long long tr2;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
-        trace[4LL * it + 0] = tr0;
-        trace[4LL * it + 1] = trg;  // no separate critical poll: values in hand
-        trace[4LL * it + 2] = tr2;
-        trace[4LL * it + 3] = min(rounds, 1023);
-    }
     __syncwarp();
     if (reset && active && gl < BS) reset[(PAD ? 4 * static_cast<int64_t>(m.blk) : r0) + gl] = pending_value();
 }
 
-template <int LG, int BS, bool UPPER, bool PAD = false, bool RAX = false>
+template <int LG, int BS, bool UPPER, bool PAD = false>
 __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restrict__ srec, const int32_t* __restrict__ bcol,
                                           const double* __restrict__ vals, const double* __restrict__ invd,
                                           const double* rhs, double* out, double* reset, int64_t warp,
-                                          int64_t nwarps, int tune, long long* trace, RUpdate ru = RUpdate{}) {
-    // tune: sleep_ns << 8 | experiment bits (developer timing probes that
-    // give WRONG results: 1 = matrix values from one cached line, 2 = no
-    // dependency waits, 4 = no dependency loads at all)
-    const unsigned sleep_ns = static_cast<unsigned>(tune >> 8);
+                                          int64_t nwarps) {
     constexpr int G = 32 / LG;
     constexpr int RS = PAD && UPPER ? 4 : BS;  // right-hand side stride (padded y)
-    const double alpha = RAX ? *ru.alpha : 0.0;
-    // right-hand side entry i (RAX: r_new = r - alpha q, as k_axpy forms it)
-    auto rhs_at = [&](int64_t i) { return RAX ? fma(-alpha, ru.q[i], rhs[i]) : rhs[i]; };
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     // 32-bit item indices (items * G < 2^31, checked by the launcher)
@@ -716,17 +620,6 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
     BsrSlot m = bsr_slot32(it, nit, G, grp, srec);
     BsrSlot m1 = bsr_slot32(it + nw, nit, G, grp, srec);
     BsrSlot m2 = bsr_slot32(it + 2 * nw, nit, G, grp, srec);
-#if BSR_PF >= 2
-    BsrSlot m3 = bsr_slot32(it + 3 * nw, nit, G, grp, srec);
-#endif
-#if BSR_RHS_AHEAD
-    double rhs0[BS], rhs1[BS];
-#pragma unroll
-    for (int t = 0; t < BS; ++t) {
-        rhs0[t] = m.blk >= 0 ? rhs_at(static_cast<int64_t>(m.blk) * RS + t) : 0.0;
-        rhs1[t] = m1.blk >= 0 ? rhs_at(static_cast<int64_t>(m1.blk) * RS + t) : 0.0;
-    }
-#endif
     // one 128-byte line per lane covers a block's rows up to 16 * LG
     // doubles (3 elasticity rows: ~125); longer rows take the loop
     auto prefetch = [&](const BsrSlot& q) {
@@ -744,25 +637,13 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             }
         }
     };
-#if BSR_PF >= 1
     prefetch(m);
-#endif
-#if BSR_PF >= 2
-    prefetch(m1);
-#endif
     while (it < nit) {
-#if BSR_PF >= 2
-        prefetch(m2);
-#elif BSR_PF == 1
         prefetch(m1);
-#endif
-        long long tr0 = 0;
-        if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
-#if !BSR_RHS_AHEAD
         // loaded as the item starts: only the diagonal solve (after the
         // dependency polls) consumes it
         double rhs0[BS];
-        if constexpr (RS == 4 && !RAX) {  // padded y: one 256-bit load
+        if constexpr (RS == 4) {  // padded y: one 256-bit load
             double d3 = 0.0;
             rhs0[0] = rhs0[1] = rhs0[2] = 0.0;
             if (m.blk >= 0)
@@ -772,268 +653,26 @@ __device__ __forceinline__ void bsr_sweep(int64_t nitems, const int32_t* __restr
             (void)d3;
         } else {
 #pragma unroll
-            for (int t = 0; t < BS; ++t) rhs0[t] = m.blk >= 0 ? rhs_at(static_cast<int64_t>(m.blk) * RS + t) : 0.0;
+            for (int t = 0; t < BS; ++t) rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
         }
-#endif
-        bsr_item<LG, BS, UPPER, PAD, RAX>(m, rhs0, bcol, vals, invd, out, reset, sleep_ns, tune & 0xff, it, trace, tr0,
-                                          ru.rnew);
+        bsr_item<LG, BS, UPPER, PAD>(m, rhs0, bcol, vals, invd, out, reset);
         it += nw;
         m = m1;
         m1 = m2;
-#if BSR_PF >= 2
-        m2 = m3;
-        m3 = bsr_slot32(it + 3 * nw, nit, G, grp, srec);
-#else
         m2 = bsr_slot32(it + 2 * nw, nit, G, grp, srec);
-#endif
-#if BSR_RHS_AHEAD
-#pragma unroll
-        for (int t = 0; t < BS; ++t) {
-            rhs0[t] = rhs1[t];
-            rhs1[t] = m1.blk >= 0 ? rhs_at(static_cast<int64_t>(m1.blk) * RS + t) : 0.0;
-        }
-#endif
     }
 }
 
-// DEV: developer probes (tune word, per-item trace) compiled in; the
-// production instantiation drops their branches and registers.
-template <int LG, int BS, bool UPPER, bool PAD, bool RAX = false, bool DEV = false>
+template <int LG, int BS, bool UPPER, bool PAD>
 __global__ void __launch_bounds__(BSR_THREADS, BSR_CTAS)
 bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                 const int32_t* __restrict__ bcol, const double* __restrict__ vals,
                 const double* __restrict__ invd, const double* rhs, double* out, double* reset,
-                const int* __restrict__ done, int tune, long long* trace, RUpdate ru) {
+                const int* __restrict__ done) {
     if (done && *done) return;
-    bsr_sweep<LG, BS, UPPER, PAD, RAX>(nitems, srec, bcol, vals, invd, rhs, out, reset,
-                                       (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
-                                       (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, DEV ? tune : 0,
-                                       DEV ? trace : nullptr, ru);
-}
-
-// ------------------------------------------------------------------------
-// Tiled node-blocked sweep (TileSched). CTA c owns contiguous ranges of
-// block rows and runs them in (level, index) order, items dealt round-robin
-// to its warps exactly like bsr_sweep. A block's result goes to L2 (for the
-// other CTAs and the caller) and into a shared-memory ring slot indexed by
-// its list position, so a dependency owned by the same CTA -- most of them
-// for a contiguous range -- is read from shared memory (~tens of ns) instead
-// of a round trip through L2 (~1 us under the sweep's load). The slot is a
-// seqlock: {tag, values}; the writer sets tag = -1, fences, writes the
-// values, fences, sets tag = position. A reader accepts the values when the
-// tag equals the dependency's position before and after reading them; a tag
-// beyond it means the slot was recycled and the value is read from L2.
-struct __align__(16) TileSlot {
-    int tag;
-    int pad;
-    double v[3];
-};
-
-__device__ __forceinline__ int lds_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-
-template <int LG, int BS, bool UPPER, int RING>
-__global__ void __launch_bounds__(512, 1)
-tile_trsv_kernel(const int64_t* __restrict__ tbeg, const int32_t* __restrict__ tsrec,
-                 const uint32_t* __restrict__ tcol,
-                 const double* __restrict__ vals, const double* __restrict__ invd, const double* rhs, double* out,
-                 double* reset, const int* __restrict__ done) {
-    static_assert(BS <= 3, "ring slots hold 3 values");
-    extern __shared__ __align__(16) unsigned char tile_smem[];
-    TileSlot* ring = reinterpret_cast<TileSlot*>(tile_smem);
-    if (done && *done) return;
-    for (int i = threadIdx.x; i < RING; i += blockDim.x) ring[i].tag = -1;
-    __syncthreads();
-    constexpr int G = 32 / LG;
-    constexpr int NIB = BS * (BS - 1) / 2;
-    constexpr uint32_t DMASK = (1u << kTileDistBits) - 1;
-    const int lane = threadIdx.x & 31;
-    const int grp = lane / LG, gl = lane % LG;
-    const int64_t base = tbeg[blockIdx.x];
-    const int64_t nitems = (tbeg[blockIdx.x + 1] - base) / G;
-    const int32_t* srec = tsrec + 4 * base;
-    const int64_t nwarps = blockDim.x >> 5;
-    int64_t it = threadIdx.x >> 5;
-    BsrSlot m = bsr_slot(it, nitems, G, grp, srec);
-    BsrSlot m1 = bsr_slot(it + nwarps, nitems, G, grp, srec);
-    BsrSlot m2 = bsr_slot(it + 2 * nwarps, nitems, G, grp, srec);
-    BsrSlot m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
-    double rhs0[BS], rhs1[BS];
-#pragma unroll
-    for (int t = 0; t < BS; ++t) {
-        rhs0[t] = m.blk >= 0 ? rhs[static_cast<int64_t>(m.blk) * BS + t] : 0.0;
-        rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
-    }
-    auto prefetch = [&](const BsrSlot& q) {
-        if (q.blk >= 0) {
-            int64_t rq[BS + 1];
-            slot_rows<BS>(q, rq);
-            const int64_t e0 = rq[0], e1 = rq[BS];
-            for (int64_t a = (e0 & ~15LL) + 16 * gl; a < e1; a += 16 * LG)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + a));
-            if (gl == 0) {
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(tcol + q.bp));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(invd + static_cast<int64_t>(q.blk) * BS));
-            }
-        }
-    };
-    auto first_code = [&](const BsrSlot& q) {
-        return gl < slot_nb<BS, UPPER>(q) ? ld_stream(reinterpret_cast<const int32_t*>(tcol) + q.bp + gl) : 0;
-    };
-    prefetch(m);
-    prefetch(m1);
-    int32_t code0 = first_code(m), code1 = first_code(m1);
-    while (it < nitems) {
-        prefetch(m2);
-        const bool active = m.blk >= 0;
-        const int64_t r0 = active ? static_cast<int64_t>(m.blk) * BS : 0;
-        const int pos = static_cast<int>(it * G + grp);  // position in this CTA's list
-        int64_t mrp[BS + 1];
-        slot_rows<BS>(m, mrp);
-        int64_t ob[BS];
-#pragma unroll
-        for (int t = 0; t < BS; ++t) ob[t] = UPPER ? mrp[t] + (BS - t) : mrp[t];
-        const int nb = active ? static_cast<int>((UPPER ? mrp[1] - ob[0] : mrp[1] - 1 - mrp[0]) / BS) : 0;
-        double binv[BS], bin[NIB > 0 ? NIB : 1];
-        if (active && gl == 0) {
-#pragma unroll
-            for (int t = 0; t < BS; ++t) binv[t] = __ldg(invd + r0 + t);
-            int q = 0;
-#pragma unroll
-            for (int t = 0; t < BS; ++t)
-#pragma unroll
-                for (int s = 0; s < BS; ++s) {
-                    if (!UPPER && s < t) bin[q++] = ld_stream(vals + mrp[t + 1] - (t + 1) + s);
-                    if (UPPER && s > t) bin[q++] = ld_stream(vals + mrp[t] + (s - t));
-                }
-        }
-        double acc[BS];
-#pragma unroll
-        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
-        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
-        for (int n0 = 0; n0 < nbmax; n0 += LG) {
-            const int n = n0 + gl;
-            const bool own = n < nb;
-            double a[BS][BS], xv[BS];
-            int64_t xc = 0;
-            int target = -1;  // >= 0: read the ring slot of this position
-            bool need = false;
-#pragma unroll
-            for (int t = 0; t < BS; ++t) xv[t] = 0.0;
-            if (own) {
-                const uint32_t code = static_cast<uint32_t>(
-                    n0 == 0 ? code0 : ld_stream(reinterpret_cast<const int32_t*>(tcol) + m.bp + n));
-                xc = static_cast<int64_t>(code >> kTileDistBits) * BS;
-                const int d = static_cast<int>(code & DMASK);
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) a[t][c] = ld_stream(vals + ob[t] + BS * n + c);
-                if (d) {
-                    target = pos - d;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) xv[c] = ld_relaxed(out + xc + c);
-                }
-                need = true;
-            } else {
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) a[t][c] = 0.0;
-            }
-            while (__any_sync(0xffffffffu, need)) {
-                if (need) {
-                    if (target >= 0) {
-                        TileSlot* sl = ring + (target & (RING - 1));
-                        const int t1 = lds_volatile(&sl->tag);
-                        if (t1 == target) {
-                            __threadfence_block();
-                            double w[BS];
-#pragma unroll
-                            for (int c = 0; c < BS; ++c) w[c] = *reinterpret_cast<volatile double*>(&sl->v[c]);
-                            __threadfence_block();
-                            const int t2 = lds_volatile(&sl->tag);
-                            if (t2 == target) {
-#pragma unroll
-                                for (int c = 0; c < BS; ++c) xv[c] = w[c];
-                                need = false;
-                            } else if (t2 > target) {
-                                target = -1;  // recycled: the value is in L2
-#pragma unroll
-                                for (int c = 0; c < BS; ++c) xv[c] = pending_value();
-                            }
-                        } else if (t1 > target) {
-                            target = -1;
-#pragma unroll
-                            for (int c = 0; c < BS; ++c) xv[c] = pending_value();
-                        }
-                    } else {
-                        bool pend = false;
-#pragma unroll
-                        for (int c = 0; c < BS; ++c)
-                            if (is_pending(xv[c])) {
-                                xv[c] = ld_relaxed(out + xc + c);
-                                pend |= is_pending(xv[c]);
-                            }
-                        need = pend;
-                    }
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < BS; ++t)
-#pragma unroll
-                for (int c = 0; c < BS; ++c) acc[t] = fma(a[t][c], xv[c], acc[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
-        if (active && gl == 0) {
-            double xb[BS];
-            if (!UPPER) {
-                int q = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    double s = rhs0[t] - acc[t];
-#pragma unroll
-                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            } else {
-#pragma unroll
-                for (int t = BS - 1; t >= 0; --t) {
-                    double s = rhs0[t] - acc[t];
-                    int q = 0;
-#pragma unroll
-                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            }
-            TileSlot* sl = ring + (pos & (RING - 1));
-            *reinterpret_cast<volatile int*>(&sl->tag) = -1;
-            __threadfence_block();
-#pragma unroll
-            for (int t = 0; t < BS; ++t) *reinterpret_cast<volatile double*>(&sl->v[t]) = xb[t];
-            __threadfence_block();
-            *reinterpret_cast<volatile int*>(&sl->tag) = pos;
-#pragma unroll
-            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
-        }
-        __syncwarp();
-        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
-        it += nwarps;
-        m = m1;
-        m1 = m2;
-        m2 = m3;
-        m3 = bsr_slot(it + 3 * nwarps, nitems, G, grp, srec);
-        code0 = code1;
-        code1 = first_code(m1);
-#pragma unroll
-        for (int t = 0; t < BS; ++t) {
-            rhs0[t] = rhs1[t];
-            rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
-        }
-    }
+    bsr_sweep<LG, BS, UPPER, PAD>(nitems, srec, bcol, vals, invd, rhs, out, reset,
+                                  (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                                  (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
 }
 
 // Round-robin sweep for matrices that are not node-blocked (Poisson, FV
@@ -1042,8 +681,7 @@ tile_trsv_kernel(const int64_t* __restrict__ tbeg, const int32_t* __restrict__ t
 // one item ahead, dependency values polled directly -- with lanes over the
 // block's off-block entries (lane gl takes entries gl, gl + LG, ... of the
 // block's rows in order) instead of over neighbour blocks.
-// RR_THREADS-thread CTAs, RR_CTAS resident per SM; DEV: the poll back-off
-// knob compiled in (the production build drops it)
+// RR_THREADS-thread CTAs, RR_CTAS resident per SM
 // (diffusion 256^3, per sweep: 256 x 4/SM 1.18 ms, 128 x 9/SM 1.15, 128 x 12/SM 1.28)
 #ifndef RR_THREADS
 #define RR_THREADS 128
@@ -1051,15 +689,14 @@ tile_trsv_kernel(const int64_t* __restrict__ tbeg, const int32_t* __restrict__ t
 #ifndef RR_CTAS
 #define RR_CTAS 9
 #endif
-template <int LG, int BS, bool UPPER, int CH, bool DEV = false>
+template <int LG, int BS, bool UPPER, int CH>
 __global__ void __launch_bounds__(RR_THREADS, RR_CTAS)
 rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                const int32_t* __restrict__ cols, const double* __restrict__ vals, const double* __restrict__ invd,
-               const double* rhs, double* out, double* reset, const int* __restrict__ done, int tune) {
+               const double* rhs, double* out, double* reset, const int* __restrict__ done) {
     if (done && *done) return;
     constexpr int G = 32 / LG;
     constexpr int NIB = BS * (BS - 1) / 2;
-    const unsigned sleep_ns = DEV ? static_cast<unsigned>(tune >> 8) : 0u;
     const int lane = threadIdx.x & 31;
     const int grp = lane / LG, gl = lane % LG;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -1152,7 +789,6 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
 #pragma unroll
             for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
             while (__any_sync(0xffffffffu, pend)) {
-                if (sleep_ns) __nanosleep(sleep_ns);
                 pend = false;
 #pragma unroll
                 for (int c = 0; c < CH; ++c)
@@ -1171,27 +807,7 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
         for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
         if (active && gl == 0) {
             double xb[BS];
-            if (!UPPER) {
-                int q = 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t) {
-                    double s = rhs0[t] - acc[t];
-#pragma unroll
-                    for (int u = 0; u < t; ++u) s -= bin[q++] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            } else {
-#pragma unroll
-                for (int t = BS - 1; t >= 0; --t) {
-                    double s = rhs0[t] - acc[t];
-                    int q = 0;
-#pragma unroll
-                    for (int r = 0; r < t; ++r) q += BS - 1 - r;
-#pragma unroll
-                    for (int u = t + 1; u < BS; ++u) s -= bin[q + (u - t - 1)] * xb[u];
-                    xb[t] = s * binv[t];
-                }
-            }
+            solve_diag_block<BS, UPPER>(rhs0, acc, bin, binv, xb);
 #pragma unroll
             for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
         }
@@ -1208,145 +824,6 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
             rhs1[t] = m1.blk >= 0 ? rhs[static_cast<int64_t>(m1.blk) * BS + t] : 0.0;
         }
     }
-}
-
-// w = A z for node-blocked A, following the backward sweep's frontier: a
-// warp takes two block rows (in the order their z inputs complete,
-// Analysis::mv_order), lane n owns neighbour block n of both, polls its z
-// values like a sweep item and the warp writes the 2 x BS products. The
-// next pair's row pointers are loaded one pair ahead.
-template <int BS>
-struct MvMeta {
-    int64_t blk[2];
-    int64_t rp[2][BS + 1];
-};
-
-template <int BS>
-__device__ __forceinline__ MvMeta<BS> mv_meta(unsigned c, int64_t nb, const int32_t* __restrict__ order,
-                                              const int64_t* __restrict__ arp) {
-    MvMeta<BS> m;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t k = 2 * static_cast<int64_t>(c) + j;
-        m.blk[j] = k < nb ? static_cast<int64_t>(__ldg(order + k)) : -1;
-#pragma unroll
-        for (int t = 0; t <= BS; ++t) m.rp[j][t] = m.blk[j] >= 0 ? __ldg(arp + m.blk[j] * BS + t) : 0;
-    }
-    return m;
-}
-
-template <int BS>
-__device__ __forceinline__ void bsr_mv(int64_t nb, const int32_t* __restrict__ order,
-                                       const int64_t* __restrict__ arp, const int32_t* __restrict__ acols,
-                                       const double* __restrict__ avals, const double* z, double* __restrict__ w,
-                                       unsigned* counter) {
-    const int lane = threadIdx.x & 31;
-    const int64_t npairs = (nb + 1) / 2;
-    unsigned c = 0, cn = 0;
-    if (lane == 0) {
-        c = atomicAdd(counter, 1u);
-        cn = atomicAdd(counter, 1u);
-    }
-    c = __shfl_sync(0xffffffffu, c, 0);
-    cn = __shfl_sync(0xffffffffu, cn, 0);
-    MvMeta<BS> m = mv_meta<BS>(c, nb, order, arp);
-    MvMeta<BS> mn = mv_meta<BS>(cn, nb, order, arp);
-    while (c < npairs) {
-        unsigned after = 0;
-        if (lane == 0) after = atomicAdd(counter, 1u);
-        int nbk[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) nbk[j] = m.blk[j] >= 0 ? static_cast<int>((m.rp[j][1] - m.rp[j][0]) / BS) : 0;
-        const int nbmax = max(nbk[0], nbk[1]);
-        double acc[2][BS];
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int t = 0; t < BS; ++t) acc[j][t] = 0.0;
-        for (int n0 = 0; n0 < nbmax; n0 += 32) {
-            const int n = n0 + lane;
-            double a[2][BS][BS], xv[2][BS];
-            int32_t xc[2];
-            bool own[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                own[j] = n < nbk[j];
-                xc[j] = own[j] ? ld_stream(acols + m.rp[j][0] + BS * n) : 0;
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int cc = 0; cc < BS; ++cc)
-                        a[j][t][cc] = own[j] ? ld_stream(avals + m.rp[j][t] + BS * n + cc) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int cc = 0; cc < BS; ++cc) xv[j][cc] = own[j] ? ld_relaxed(z + xc[j] + cc) : 0.0;
-            bool pend = false;
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int cc = 0; cc < BS; ++cc) pend |= own[j] && is_pending(xv[j][cc]);
-            while (__any_sync(0xffffffffu, pend)) {
-                pend = false;
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int cc = 0; cc < BS; ++cc)
-                        if (own[j] && is_pending(xv[j][cc])) {
-                            xv[j][cc] = ld_relaxed(z + xc[j] + cc);
-                            pend |= is_pending(xv[j][cc]);
-                        }
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int t = 0; t < BS; ++t)
-#pragma unroll
-                    for (int cc = 0; cc < BS; ++cc) acc[j][t] = fma(a[j][t][cc], xv[j][cc], acc[j][t]);
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int t = 0; t < BS; ++t) acc[j][t] = group_sum<32>(acc[j][t]);
-        if (lane == 0) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-                if (m.blk[j] >= 0)
-#pragma unroll
-                    for (int t = 0; t < BS; ++t) w[m.blk[j] * BS + t] = acc[j][t];
-        }
-        after = __shfl_sync(0xffffffffu, after, 0);
-        c = cn;
-        m = mn;
-        cn = after;
-        mn = mv_meta<BS>(after, nb, order, arp);
-    }
-}
-
-// Backward sweep z = U^-1 y and w = A z in one launch. The first `nsweep`
-// CTAs to start (ticket counter[1]) run the sweep (nsweep must fit on the
-// GPU at once); the rest run the product on counter[2]. Product warps only
-// wait on sweep items, and the sweep CTAs are the first ones resident.
-template <int LG, int BS>
-__global__ void __launch_bounds__(256, BSR_MINB)
-bsr_upper_mv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
-                    const int32_t* __restrict__ bcol, const double* __restrict__ vals,
-                    const double* __restrict__ invd, const double* rhs, double* out, double* reset,
-                    unsigned nsweep, int64_t nb, const int32_t* __restrict__ order,
-                    const int64_t* __restrict__ arp, const int32_t* __restrict__ acols,
-                    const double* __restrict__ avals, double* __restrict__ w, const int* __restrict__ done,
-                    unsigned* counters, int tune, long long* trace) {
-    if (done && *done) return;
-    __shared__ unsigned role;
-    if (threadIdx.x == 0) role = atomicAdd(counters + 1, 1u);
-    __syncthreads();
-    if (role < nsweep)
-        bsr_sweep<LG, BS, true>(nitems, srec, bcol, vals, invd, rhs, out, reset,
-                                static_cast<int64_t>(role) * (blockDim.x >> 5) + (threadIdx.x >> 5),
-                                static_cast<int64_t>(nsweep) * (blockDim.x >> 5), tune & ~0xff, trace);
-    else
-        bsr_mv<BS>(nb, order, arp, acols, avals, out, w, counters + 2);
 }
 
 // ------------------------------------------------------------------------
