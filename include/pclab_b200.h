@@ -150,7 +150,11 @@ pclab_status pclab_precond_levels(const pclab_precond* p, int32_t* level_lower,
 /* Phase timings of the build (ms): analysis, ic0, gnn, total. */
 pclab_status pclab_precond_timings(const pclab_precond* p, double* ms4);
 
-/* PCG with a built preconditioner; b and x are DEVICE pointers. */
+/* PCG with a built preconditioner; b and x are DEVICE pointers. A non-NULL
+ * `stream` (cudaStream_t) is used for this call only; NULL runs on the
+ * library stream (pclab_set_stream). The preconditioner co-owns the matrix
+ * analysis its factor lives on, so it stays usable after
+ * pclab_matrix_drop_analysis. */
 pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p,
                                     const double* b, double* x, double rel_tol,
                                     int64_t max_iters, int record_history,
@@ -158,20 +162,21 @@ pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p,
 
 /* Per-kernel device times of the PCG loop: runs up to max_iters eager
  * iterations (rel_tol 1e-300) with a CUDA event between kernels and writes
- * ms8 = [k0, axpy+norm, sweep L, k3, dot, iterations, fused, 0] where
- * fused = 0: k0 = p-update + A p (+ pAp), k3 = sweep L^T;
- * fused = 1: k0 = p/q update + pq, k3 = sweep L^T fused with w = A z. */
+ * ms8 = [p-update + A p (+ pAp), axpy + norm, sweep L, sweep L^T, dot,
+ * iterations, 0, 0]. */
 pclab_status pclab_pcg_profile(pclab_matrix* a, const pclab_precond* p, const double* b,
                                double* x, int64_t max_iters, double* ms8);
 
 /* Run all subsequent library work on `stream` (a cudaStream_t; NULL
- * restores the library's private stream). */
+ * restores the library's private stream). This is the only sticky stream
+ * setter: the `stream` argument of the *_device calls applies to that call
+ * alone. */
 void pclab_set_stream(void* stream);
 
 /* Kernel launches issued by the library so far (graph nodes included). */
 long long pclab_launch_count(void);
 
-/* Individual kernels on device vectors. */
+/* Individual kernels on device vectors (`stream`: this call only). */
 pclab_status pclab_spmv_device(const pclab_matrix* a, const double* x, double* y,
                                void* stream);
 /* upper != 0 solves L^T x = b, else L x = b, with p's factor. */

@@ -364,8 +364,10 @@ def pcg(a: Csr, b: np.ndarray, kind: str = "ic0", params: np.ndarray | None = No
                   lo.rp.ctypes.data if lo else None, lo.cols.ctypes.data if lo else None,
                   lo.vals.ctypes.data if lo else None, rel_tol, max_iters, x, C.byref(rep),
                   hist.ctypes.data if hist is not None else None)
+    if st == 6:  # OR_ERR_CURVATURE: the reference's message (krylov.cpp:151-154)
+        raise OracleError(3, f"pcg: nonpositive curvature at iteration {rep.iterations} (matrix not SPD?)")
     if st:
-        raise OracleError(st, "pcg: nonpositive curvature or zero pivot")
+        raise OracleError(st, "pcg: zero pivot in the triangular solve")
     r = {k: getattr(rep, k) for k, _ in OrReport._fields_}
     if history:
         return x, r, hist[: rep.iterations + 1]

@@ -832,7 +832,8 @@ int or_pcg(int64_t n, const int64_t* rp, const int32_t* cols, const double* vals
             or_csr_matvec(n, rp, cols, vals, pv, ap);
             const double pap = dot(n, pv, ap);
             if (!(pap > 0.0)) {
-                st = OR_ERR_NUMERIC;
+                rep->iterations = k;
+                st = OR_ERR_CURVATURE;
                 break;
             }
             const double alpha = rz / pap;

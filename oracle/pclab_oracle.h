@@ -29,7 +29,9 @@
 extern "C" {
 #endif
 
-enum { OR_OK = 0, OR_ERR_ARGUMENT = 1, OR_ERR_FORMAT = 2, OR_ERR_NUMERIC = 3 };
+enum { OR_OK = 0, OR_ERR_ARGUMENT = 1, OR_ERR_FORMAT = 2, OR_ERR_NUMERIC = 3,
+       /* or_pcg: p^T A p <= 0 (krylov.cpp:151-154); rep->iterations = the failing k */
+       OR_ERR_CURVATURE = 6 };
 
 /* ---- counter-based RNG (reference rng.hpp) ---- */
 uint64_t or_mix64(uint64_t x);

@@ -422,13 +422,9 @@ __global__ void items_fill(int32_t nl, int64_t nb, int per_item, const int64_t* 
     }
 }
 
-template <class T>
-T dev_read(const T* d, cudaStream_t st) {
-    T v;
-    CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return v;
-}
+inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
 
 void scan_inplace(int64_t* p, int64_t n, cudaStream_t st) {
     size_t tmp = 0;
@@ -438,9 +434,6 @@ void scan_inplace(int64_t* p, int64_t n, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
 }
 
-inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
-
-}  // namespace
 
 void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
                     cudaStream_t st, const BlockCols* pbc, const BlockCols* sbc) {
@@ -574,7 +567,7 @@ static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool 
     CK(cudaStreamSynchronize(st));
 }
 
-static void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, cudaStream_t st) {
+void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, cudaStream_t st) {
     const int64_t nb = M.n / bs;
     bc.bp.alloc(nb + 1);
     if (nb > 0) {
@@ -720,6 +713,8 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
             }
         }
     }
+    // range-pipelined sweeps (range.cu) on the final sweep layout
+    build_range_scheds(*an, st);
     // node-blocked A: the PCG product reads one column index per block
     an->a_bsr = false;
     if (an->bsr) {

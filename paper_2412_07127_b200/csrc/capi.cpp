@@ -20,7 +20,6 @@ using namespace pclab_b200;
 
 struct pclab_matrix {
     std::unique_ptr<Matrix> m;
-    int64_t n_cols = 0;
 };
 struct pclab_model {
     Model m;
@@ -31,8 +30,10 @@ struct pclab_precond {
 
 namespace pclab_b200 {
 
-static cudaStream_t g_user_stream = nullptr;
+static cudaStream_t g_user_stream = nullptr;  // pclab_set_stream (sticky, documented)
 static bool g_user_stream_set = false;
+// a stream passed to one *_device call: used for that call only
+static thread_local cudaStream_t t_call_stream = nullptr;
 
 void* dev_alloc(size_t bytes) {
     static bool pool_ready = [] {
@@ -62,6 +63,7 @@ void dev_free(void* p) { cudaFreeAsync(p, lib_stream()); }
 // (e.g. the caller's current stream, so its events bracket our work), else
 // a private non-blocking stream.
 cudaStream_t lib_stream() {
+    if (t_call_stream) return t_call_stream;
     if (g_user_stream_set) return g_user_stream;
     static cudaStream_t s = [] {
         cudaStream_t t;
@@ -149,15 +151,18 @@ char* dup_string(const std::string& s) {
     return p;
 }
 
-// A stream passed to a device entry point becomes the library stream, so
-// stream-ordered temporaries and the kernels that use them share one order.
-cudaStream_t as_stream(void* s) {
-    if (s) {
-        g_user_stream = static_cast<cudaStream_t>(s);
-        g_user_stream_set = true;
+// A stream passed to a device entry point is the library stream for that
+// call only (stream-ordered temporaries and the kernels that use them share
+// one order); the previous stream is restored when the call returns.
+struct CallStream {
+    cudaStream_t prev;
+    explicit CallStream(void* s) : prev(t_call_stream) {
+        if (s) t_call_stream = static_cast<cudaStream_t>(s);
     }
-    return lib_stream();
-}
+    ~CallStream() { t_call_stream = prev; }
+    CallStream(const CallStream&) = delete;
+    CallStream& operator=(const CallStream&) = delete;
+};
 
 std::string entry_str(int64_t i, int64_t j) {
     return "(" + std::to_string(i) + ", " + std::to_string(j) + ")";
@@ -194,7 +199,7 @@ std::unique_ptr<Matrix> coo_upload(int64_t n_rows, int64_t n_cols, int64_t nnz, 
         v[k] = vals[s];
     }
     for (int64_t i = 0; i < n_rows; ++i) rp[i + 1] += rp[i];
-    return matrix_from_csr_device(n_rows, nnz, rp.data(), c.data(), v.data(), lib_stream());
+    return matrix_from_csr_device(n_rows, nnz, rp.data(), c.data(), v.data(), lib_stream(), n_cols);
 }
 
 // -------------------------------------------------- Matrix Market (host IO)
@@ -273,7 +278,6 @@ pclab_matrix* mm_read(const std::string& path) {
     } catch (const FormatError& e) {
         throw FormatError(std::string("matrix market: ") + e.what());
     }
-    h->n_cols = nc;
     return h.release();
 }
 
@@ -297,14 +301,14 @@ void mm_write(const pclab_matrix* a, const std::string& path) {
     std::vector<double> v;
     download_csr(*a->m, rp, c, v);
     const int64_t n = a->m->a.n;
-    const bool symmetric = n == a->n_cols && matrix_symmetric(*a->m, lib_stream());
+    const bool symmetric = n == a->m->n_cols && matrix_symmetric(*a->m, lib_stream());
     std::ofstream out(path);
     if (!out) throw IoError("cannot open '" + path + "' for writing");
     out << "%%MatrixMarket matrix coordinate real " << (symmetric ? "symmetric" : "general") << "\n";
     int64_t cnt = 0;
     for (int64_t i = 0; i < n; ++i)
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) cnt += !symmetric || c[k] <= i;
-    out << n << " " << a->n_cols << " " << cnt << "\n";
+    out << n << " " << a->m->n_cols << " " << cnt << "\n";
     char buf[64];
     for (int64_t i = 0; i < n; ++i)
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
@@ -429,7 +433,6 @@ pclab_status pclab_matrix_from_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, 
     return guarded([&] {
         auto h = std::make_unique<pclab_matrix>();
         h->m = coo_upload(n_rows, n_cols, nnz, rows, cols, values);
-        h->n_cols = n_cols;
         *out = h.release();
     });
 }
@@ -442,7 +445,6 @@ pclab_status pclab_matrix_from_csr(int64_t n, int64_t nnz, const int64_t* row_pt
     return guarded([&] {
         auto h = std::make_unique<pclab_matrix>();
         h->m = matrix_from_csr_device(n, nnz, row_ptr, cols, vals, lib_stream());
-        h->n_cols = n;
         *out = h.release();
     });
 }
@@ -454,7 +456,6 @@ pclab_status pclab_matrix_gen_poisson(int dim, int64_t m, int variable_coeff, ui
     return guarded([&] {
         auto h = std::make_unique<pclab_matrix>();
         h->m = gen_poisson_device(dim, m, nullptr, lib_stream());
-        h->n_cols = h->m->a.n;
         *out = h.release();
     });
 }
@@ -472,7 +473,6 @@ pclab_status pclab_matrix_gen_diffusion(int dim, int64_t m, double lo, double hi
         for (int64_t c = 0; c < n; ++c) k[c] = std::pow(10.0, lo + (hi - lo) * uniform_at(seed, c));
         auto h = std::make_unique<pclab_matrix>();
         h->m = gen_poisson_device(dim, m, k.data(), lib_stream());
-        h->n_cols = n;
         *out = h.release();
     });
 }
@@ -483,7 +483,6 @@ pclab_status pclab_matrix_gen_elasticity(int64_t m, double nu, const double* mod
     return guarded([&] {
         auto h = std::make_unique<pclab_matrix>();
         h->m = gen_elasticity_device(m, nu, moduli, lib_stream());
-        h->n_cols = h->m->a.n;
         *out = h.release();
     });
 }
@@ -491,7 +490,7 @@ pclab_status pclab_matrix_gen_elasticity(int64_t m, double nu, const double* mod
 pclab_status pclab_matrix_shape(const pclab_matrix* a, int64_t* n_rows, int64_t* n_cols, int64_t* nnz) {
     if (a == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_matrix_shape: null matrix");
     if (n_rows) *n_rows = a->m->a.n;
-    if (n_cols) *n_cols = a->n_cols;
+    if (n_cols) *n_cols = a->m->n_cols;
     if (nnz) *nnz = a->m->a.nnz;
     return PCLAB_OK;
 }
@@ -601,7 +600,6 @@ pclab_status pclab_precond_build(pclab_matrix* a, const char* kind, const pclab_
     if (a == nullptr || kind == nullptr || out == nullptr)
         return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_build: null argument");
     return guarded([&] {
-        if (a->m->a.n != a->n_cols) throw DimensionError("matrix not square");
         auto h = std::make_unique<pclab_precond>();
         h->p = build_precond(*a->m, parse_kind(kind), model ? &model->m : nullptr, lib_stream());
         *out = h.release();
@@ -613,7 +611,7 @@ void pclab_precond_free(pclab_precond* p) { delete p; }
 pclab_status pclab_precond_info(const pclab_precond* p, int64_t* nnz_lower, int32_t* block_size,
                                 int32_t* levels_lower, int32_t* levels_upper, double* sigma) {
     if (p == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_info: null argument");
-    const Analysis* an = p->p->a->an.get();
+    const Analysis* an = p->p->an.get();
     const bool factor = p->p->kind == Kind::IC0 || p->p->kind == Kind::NIC || p->p->kind == Kind::GnnIC;
     if (nnz_lower) *nnz_lower = factor && an ? an->lower.nnz : 0;
     if (block_size) *block_size = factor && an ? an->bs : 0;
@@ -625,7 +623,7 @@ pclab_status pclab_precond_info(const pclab_precond* p, int64_t* nnz_lower, int3
 
 pclab_status pclab_precond_layout(const pclab_precond* p, int64_t* out8) {
     if (p == nullptr || out8 == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_layout: null argument");
-    const Analysis* an = p->p->a->an.get();
+    const Analysis* an = p->p->an.get();
     for (int k = 0; k < 8; ++k) out8[k] = 0;
     if (!an) return PCLAB_OK;
     out8[0] = an->bsr ? 1 : 0;
@@ -654,9 +652,8 @@ pclab_status pclab_precond_levels(const pclab_precond* p, int32_t* lo, int32_t* 
                                   int32_t* nup) {
     if (p == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_precond_levels: null argument");
     return guarded([&] {
-        Matrix* m = const_cast<Matrix*>(p->p->a);
-        if (!m->an) throw DimensionError("preconditioner has no factor");
-        Analysis& an = *m->an;
+        if (!p->p->an) throw DimensionError("preconditioner has no factor");
+        Analysis& an = *p->p->an;
         cudaStream_t st = lib_stream();
         if (an.row_lo.level.n == 0 && an.lower.n > 0)
             compute_levels(an.lower, an.upper, 1, false, an.row_lo, st);
@@ -720,8 +717,8 @@ pclab_status pclab_pcg_solve_device(pclab_matrix* a, const pclab_precond* p, con
         return fail(PCLAB_ERR_ARGUMENT, "pclab_pcg_solve_device: null argument");
     return guarded([&] {
         if (p->p->a != a->m.get()) throw DimensionError("preconditioner built for another matrix");
-        const SolveReport r = pcg_solve(*a->m, *p->p, b, x, rel_tol, max_iters, record_history != 0,
-                                        as_stream(stream));
+        CallStream cs(stream);
+        const SolveReport r = pcg_solve(*a->m, *p->p, b, x, rel_tol, max_iters, record_history != 0, lib_stream());
         if (report_json_out) *report_json_out = dup_string(r.to_json());
     });
 }
@@ -732,7 +729,6 @@ pclab_status pclab_pcg_solve(const pclab_matrix* a, const double* b, const char*
         return fail(PCLAB_ERR_ARGUMENT, "pclab_pcg_solve: null argument");
     return guarded([&] {
         Matrix& m = *const_cast<pclab_matrix*>(a)->m;
-        if (m.a.n != a->n_cols) throw DimensionError("pcg: shape mismatch");
         cudaStream_t st = lib_stream();
         const Kind k = parse_kind(kind);
         if ((k == Kind::NIC || k == Kind::GnnIC) && model == nullptr)
@@ -752,18 +748,19 @@ pclab_status pclab_pcg_solve(const pclab_matrix* a, const double* b, const char*
 pclab_status pclab_spmv_device(const pclab_matrix* a, const double* x, double* y, void* stream) {
     if (a == nullptr || x == nullptr || y == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_spmv_device: null argument");
     return guarded([&] {
-        spmv(*a->m, x, y, as_stream(stream));
-        CK(cudaStreamSynchronize(as_stream(stream)));
+        CallStream cs(stream);
+        spmv(*a->m, x, y, lib_stream());
+        CK(cudaStreamSynchronize(lib_stream()));
     });
 }
 
 pclab_status pclab_trsv_device(const pclab_precond* p, int upper, const double* b, double* x, void* stream) {
     if (p == nullptr || b == nullptr || x == nullptr) return fail(PCLAB_ERR_ARGUMENT, "pclab_trsv_device: null argument");
     return guarded([&] {
-        const Analysis* an = p->p->a->an.get();
+        const Analysis* an = p->p->an.get();
         if (!an || p->p->lvals.n == 0) throw DimensionError("preconditioner has no factor");
-        trsv(*an, upper ? p->p->uvals.p : p->p->lvals.p, p->p->invd.p,
-             upper != 0, b, x, as_stream(stream));
+        CallStream cs(stream);
+        trsv(*an, *p->p, upper != 0, b, x, lib_stream());
     });
 }
 

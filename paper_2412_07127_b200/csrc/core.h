@@ -96,6 +96,28 @@ struct BlockCols {
     DevBuf<int32_t> bcol;  // [bp[nblocks]]
 };
 
+// Range-pipelined sweep schedule (range.cu). Nodes (blocks of bs rows) are
+// cut, in sweep order, into `nranges` contiguous ranges of `range_nodes`;
+// range r runs on CTA r % grid. Inside a range the nodes go in steps: one
+// (range, level) group, split so that a step's staged data fits a shared
+// memory stage. The per-factor stream (Precond::stream_lo / stream_up) holds
+// each step's data contiguously -- node headers, encoded neighbour columns,
+// values -- so a CTA moves one step with one bulk copy.
+struct RangeSched {
+    bool ok = false;
+    bool upper = false;
+    int bs = 1;
+    int64_t nb = 0;            // nodes
+    int64_t range_nodes = 0;   // R
+    int64_t nranges = 0, nsteps = 0;
+    int64_t stream_bytes = 0, max_step_bytes = 0;
+    DevBuf<int64_t> range_step;  // [nranges + 1] first step of each range
+    DevBuf<int4> steps;          // [nsteps] {stream offset / 16, bytes / 16, nodes, first position}
+    DevBuf<int32_t> order;       // [nb] node at each stream position
+    DevBuf<int32_t> step_of;     // [nb] step of each node
+    DevBuf<int32_t> nxt;         // [nb] first later step that reuses the node's ring slot
+};
+
 // Symbolic analysis of a structurally symmetric matrix (the reference's
 // lower_triangle + csr_transpose, sparse.cpp:137/189, done once on the
 // device): L pattern with A's lower values, U = L^T pattern, the slot map
@@ -113,16 +135,18 @@ struct Analysis {
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)
+    RangeSched rs_lo, rs_up; // range-pipelined sweeps (ok = built)
     double ms = 0.0;         // wall time of the analysis (CUDA events)
     uint64_t id = 0;         // unique per analysis (IC(0) mask cache key)
 };
 
 struct Matrix {
-    DevCsr a;
+    DevCsr a;                  // a.n rows
+    int64_t n_cols = 0;        // columns (the reference's SparseCoo::n_cols; square for every solve)
     DevBuf<int64_t> diag_pos;  // [n] position of a_ii in row i, -1 if absent
     bool symmetric_known = false, symmetric = false;
     int64_t missing_diag_row = -1;  // first row without a diagonal
-    std::unique_ptr<Analysis> an;
+    std::shared_ptr<Analysis> an;  // co-owned by the preconditioners built on it
 };
 
 struct Model {
@@ -135,10 +159,12 @@ Kind parse_kind(const std::string& s);
 
 struct Precond {
     Kind kind = Kind::None;
-    const Matrix* a = nullptr;  // borrowed
+    const Matrix* a = nullptr;  // the matrix it was built from (identity only; never dereferenced)
+    std::shared_ptr<Analysis> an;  // factor kinds: the analysis its factor lives on
     DevBuf<double> lvals;       // factor values on L's pattern
     DevBuf<double> uvals;       // same values on U's pattern (gathered)
     DevBuf<double> invd;        // 1 / l_ii (both sweeps)
+    DevBuf<unsigned char> stream_lo, stream_up;  // range-sweep streams (RangeSched)
     DevBuf<double> diag;        // Jacobi payload
     double sigma = 1.0;         // GNN edge scale
     int ic0_attempts = 0;
@@ -159,12 +185,25 @@ struct SolveReport {
 // ----------------------------------------------------------- entry points
 cudaStream_t lib_stream();
 
+// one value from device memory (synchronises the stream)
+template <class T>
+T dev_read(const T* d, cudaStream_t st) {
+    T v;
+    CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return v;
+}
+// exclusive prefix sum in place (analysis.cu)
+void scan_inplace(int64_t* p, int64_t n, cudaStream_t st);
+
 // matrices (gen.cu / capi.cpp)
 std::unique_ptr<Matrix> matrix_from_csr_host(int64_t n, const int64_t* rp, const int32_t* cols,
                                              const double* vals, cudaStream_t st);
+// rp / cols / vals may be host or device pointers; row_ptr is checked on
+// the device (rp[0] = 0, monotone, rp[n] = nnz) before any column is read
 std::unique_ptr<Matrix> matrix_from_csr_device(int64_t n, int64_t nnz, const int64_t* rp,
                                                const int32_t* cols, const double* vals,
-                                               cudaStream_t st);
+                                               cudaStream_t st, int64_t n_cols = -1);
 std::unique_ptr<Matrix> gen_poisson_device(int dim, int64_t m, const double* cell_k_host,
                                            cudaStream_t st);
 std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double* moduli_host,
@@ -174,6 +213,8 @@ bool matrix_symmetric(Matrix& a, cudaStream_t st);
 
 // analysis.cu
 Analysis& ensure_analysis(Matrix& a, cudaStream_t st);
+// block-column view; mode 0: L (diagonal last), 1: U (diagonal first), 2: A
+void build_block_cols(const DevCsr& M, int bs, int mode, BlockCols& bc, cudaStream_t st);
 void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
                     cudaStream_t st, const BlockCols* pbc = nullptr, const BlockCols* sbc = nullptr);
 
@@ -186,10 +227,19 @@ void gnn_forward(const Matrix& a, const Analysis& an, const Model& m, double* ou
 
 // kernels.cu
 void spmv(const Matrix& a, const double* x, double* y, cudaStream_t st);
-void trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b, double* x,
-          cudaStream_t st);
+struct Precond;
+void trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, cudaStream_t st);
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
                  double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false);
+// range.cu: range-pipelined sweeps
+void build_range_scheds(Analysis& an, cudaStream_t st);
+void fill_range_streams(const Analysis& an, Precond& p, cudaStream_t st);
+bool launch_range_trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x,
+                       double* reset, const int* done, cudaStream_t st, bool pad);
+void range_trace_begin(const Analysis& an, bool upper, cudaStream_t st);  // PCLAB_RANGE_TRACE
+void range_trace_end(const Analysis& an, bool upper, cudaStream_t st);
+void launch_sweep(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
+                  const int* done, unsigned* ctr, cudaStream_t st, bool pad);
 void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);
 int spmv_lanes(const Matrix& a);
 void gather_upper(const Analysis& an, const double* lvals, double* uvals, cudaStream_t st);

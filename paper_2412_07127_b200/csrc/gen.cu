@@ -113,7 +113,20 @@ __global__ void elasticity_rows(int64_t m, const double* __restrict__ moduli,
 
 // Row structure checks (SparseCoo::validate, sparse.cpp:25-43, on CSR)
 // plus the diagonal position of every row.
-__global__ void validate_rows(int64_t n, const int64_t* __restrict__ rp,
+// row_ptr shape (checked before any column is read): rp[0] = 0, monotone,
+// rp[n] = nnz; the first offending row (or n for a bad end) lands in *bad
+__global__ void rowptr_check(int64_t n, int64_t nnz, const int64_t* __restrict__ rp,
+                             unsigned long long* __restrict__ bad) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i > n) return;
+    bool ok;
+    if (i == 0) ok = rp[0] == 0;
+    else ok = rp[i] >= rp[i - 1] && rp[i] <= nnz;
+    if (i == n) ok = ok && rp[n] == nnz;
+    if (!ok) atomicMin(bad, static_cast<unsigned long long>(i));
+}
+
+__global__ void validate_rows(int64_t n, int64_t n_cols, const int64_t* __restrict__ rp,
                               const int32_t* __restrict__ cols, int64_t* __restrict__ diag_pos,
                               unsigned long long* __restrict__ bad_row,
                               unsigned long long* __restrict__ missing_diag) {
@@ -124,7 +137,7 @@ __global__ void validate_rows(int64_t n, const int64_t* __restrict__ rp,
     bool ok = e >= b;
     for (int64_t k = b; ok && k < e; ++k) {
         const int32_t j = cols[k];
-        if (j < 0 || j >= n || (k > b && cols[k - 1] >= j)) ok = false;
+        if (j < 0 || j >= n_cols || (k > b && cols[k - 1] >= j)) ok = false;
         if (j == i) dp = k;
     }
     diag_pos[i] = dp;
@@ -178,7 +191,7 @@ void matrix_validate(Matrix& a, cudaStream_t st) {
     const unsigned long long init[2] = {~0ULL, ~0ULL};
     CK(cudaMemcpyAsync(flags.p, init, sizeof init, cudaMemcpyHostToDevice, st));
     if (n > 0) {
-        validate_rows<<<(n + 255) / 256, 256, 0, st>>>(n, a.a.rp.p, a.a.cols.p, a.diag_pos.p,
+        validate_rows<<<(n + 255) / 256, 256, 0, st>>>(n, a.n_cols, a.a.rp.p, a.a.cols.p, a.diag_pos.p,
                                                        flags.p, flags.p + 1);
         CK_LAUNCH();
     }
@@ -216,6 +229,7 @@ std::unique_ptr<Matrix> gen_poisson_device(int dim, int64_t m, const double* cel
     auto mat = std::make_unique<Matrix>();
     DevCsr& a = mat->a;
     a.n = n;
+    mat->n_cols = n;
     a.rp.alloc(n + 1);
     DevBuf<double> k;
     if (cell_k_host) {
@@ -251,6 +265,7 @@ std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double
     auto mat = std::make_unique<Matrix>();
     DevCsr& a = mat->a;
     a.n = n;
+    mat->n_cols = n;
     a.rp.alloc(n + 1);
     const int T = 128;
     const unsigned g = static_cast<unsigned>((n + T - 1) / T);
@@ -270,15 +285,32 @@ std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double
 
 std::unique_ptr<Matrix> matrix_from_csr_device(int64_t n, int64_t nnz, const int64_t* rp,
                                                const int32_t* cols, const double* vals,
-                                               cudaStream_t st) {
+                                               cudaStream_t st, int64_t n_cols) {
+    if (n < 0 || nnz < 0) throw FormatError("csr: negative dimension");
+    if (n_cols < 0) n_cols = n;
+    if (n > INT32_MAX || n_cols > INT32_MAX)
+        throw FormatError("csr: dimensions exceed the int32 column index range");
     auto mat = std::make_unique<Matrix>();
     DevCsr& a = mat->a;
     a.n = n;
     a.nnz = nnz;
+    mat->n_cols = n_cols;
     a.rp.alloc(n + 1);
+    CK(cudaMemcpyAsync(a.rp.p, rp, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
+    {
+        DevBuf<unsigned long long> bad(1);
+        CK(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+        rowptr_check<<<static_cast<unsigned>((n + 1 + 255) / 256), 256, 0, st>>>(n, nnz, a.rp.p, bad.p);
+        CK_LAUNCH();
+        const unsigned long long b = read_i64(reinterpret_cast<const int64_t*>(bad.p), st);
+        if (b != ~0ULL) {
+            if (b == 0) throw FormatError("csr: row_ptr[0] != 0");
+            if (static_cast<int64_t>(b) == n) throw FormatError("csr: row_ptr[n] != nnz");
+            throw FormatError("csr: row_ptr not monotone at row " + std::to_string(b - 1));
+        }
+    }
     a.cols.alloc(nnz);
     a.vals.alloc(nnz);
-    CK(cudaMemcpyAsync(a.rp.p, rp, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st));
     if (nnz > 0) {
         CK(cudaMemcpyAsync(a.cols.p, cols, sizeof(int32_t) * nnz, cudaMemcpyDefault, st));
         CK(cudaMemcpyAsync(a.vals.p, vals, sizeof(double) * nnz, cudaMemcpyDefault, st));

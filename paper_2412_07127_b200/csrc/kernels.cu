@@ -358,8 +358,23 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, boo
     CK_LAUNCH();
 }
 
-void trsv(const Analysis& an, const double* vals, const double* invd, bool upper,
-          const double* b, double* x, cudaStream_t st) {
+// One sweep of a preconditioner: the range-pipelined kernel when its
+// schedule and stream exist (range.cu), else the round-robin / claim-based
+// sweeps above.
+void launch_sweep(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
+                  const int* done, unsigned* ctr, cudaStream_t st, bool pad) {
+    if (launch_range_trsv(an, p, upper, b, x, reset, done, st, pad)) return;
+    launch_trsv(an, upper ? p.uvals.p : p.lvals.p, p.invd.p, upper, b, x, reset, done, ctr, st, pad);
+}
+
+void trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, cudaStream_t st) {
+    range_trace_begin(an, upper, st);
+    struct TraceEnd {
+        const Analysis& an;
+        bool upper;
+        cudaStream_t st;
+        ~TraceEnd() { range_trace_end(an, upper, st); }
+    } trace_end{an, upper, st};
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
     fill_pending(x, an.lower.n, st);
@@ -377,13 +392,13 @@ void trsv(const Analysis& an, const double* vals, const double* invd, bool upper
             pad_copy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, b, b4.p, true);
             CK_LAUNCH();
         }
-        launch_trsv(an, vals, invd, upper, upper ? b4.p : b, x4.p, nullptr, nullptr, ctr.p, st, true);
+        launch_sweep(an, p, upper, upper ? b4.p : b, x4.p, nullptr, nullptr, ctr.p, st, true);
         pad_copy_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, x4.p, x, false);
         CK_LAUNCH();
         CK(cudaStreamSynchronize(st));
         return;
     }
-    launch_trsv(an, vals, invd, upper, b, x, nullptr, nullptr, ctr.p, st);
+    launch_sweep(an, p, upper, b, x, nullptr, nullptr, ctr.p, st, false);
     CK(cudaStreamSynchronize(st));
 }
 

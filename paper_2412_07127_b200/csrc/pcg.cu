@@ -517,10 +517,12 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
     const int64_t n = a.a.n;
     Timer total(st);
     if (kind == Kind::None) return p;
-    if (a.a.n != a.a.n) throw DimensionError("matrix not square");
+    // the reference's first failing check per kind (precond.cpp:92, sparse.cpp:190, features.cpp:13)
+    const bool square = a.n_cols == a.a.n;
     DevBuf<unsigned long long> bad(1);
     CK(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
     if (kind == Kind::Jacobi) {
+        if (!square) throw DimensionError("jacobi: matrix not square");
         p->diag.alloc(n);
         if (n) k_jacobi_diag<<<gfor(n), kT, 0, st>>>(n, a.a.vals.p, a.diag_pos.p, p->diag.p, bad.p);
         CK_LAUNCH();
@@ -531,6 +533,9 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
     }
     if ((kind == Kind::NIC || kind == Kind::GnnIC) && model == nullptr)
         throw DimensionError(std::string("kind '") + kind_name(kind) + "' needs a model");
+    if (!square)
+        throw DimensionError(kind == Kind::NIC ? "node_features: matrix not square"
+                                               : "lower_triangle: matrix not square");
     if (!matrix_symmetric(a, st)) throw FormatError("lower_triangle: matrix not symmetric");
     if (a.missing_diag_row >= 0) {
         if (kind == Kind::NIC)
@@ -544,6 +549,7 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
         p->ms_analysis = fresh ? a.an->ms : 0.0;
         (void)t;
     }
+    p->an = a.an;
     const Analysis& an = *a.an;
     p->lvals.alloc(an.lower.nnz);
     p->uvals.alloc(an.upper.nnz);
@@ -568,12 +574,14 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
     gather_upper(an, p->lvals.p, p->uvals.p, st);
     p->invd.alloc(n);
     reciprocal_diag(an, p->lvals.p, p->invd.p, st);
+    fill_range_streams(an, *p, st);
     p->ms_total = total.ms();  // the analysis ran inside this interval
     return p;
 }
 
 SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, double rel_tol,
                       int64_t max_iters, bool record, cudaStream_t st, double* prof_ms) {
+    if (a.n_cols != a.a.n) throw DimensionError("pcg: shape mismatch");
     if (!(rel_tol > 0.0)) throw DimensionError("pcg: rel_tol must be > 0");
     const int64_t n = a.a.n;
     if (max_iters < 0) max_iters = 10 * n;
@@ -631,15 +639,20 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         return rep;
     }
     trace("setup");
-    const Analysis* an = factor ? a.an.get() : nullptr;
-    if (factor && !an) throw DimensionError("pcg: the preconditioner's matrix analysis was dropped");
-    // padded p for the node-blocked 3x3 product
-    // (k_spmv_bsr_pap4 indexes A's entries and block columns with 32 bits)
-    const bool padp = an && an->a_bsr && an->bs == 3 && a.a.nnz < (1LL << 32) && an->abc.bcol.n < (1LL << 32);
+    // the sweeps run on the preconditioner's own analysis (co-owned: it
+    // survives pclab_matrix_drop_analysis); the product's block view is A's
+    const Analysis* an = factor ? pc.an.get() : nullptr;
+    if (factor && (!an || an->lower.n != n)) throw DimensionError("tri_solve_lower: shape mismatch");
+    const Analysis* aan = a.an ? a.an.get() : (pc.a == &a ? pc.an.get() : nullptr);
+    const bool a_bsr = aan && aan->a_bsr;
+    // padded p for the node-blocked 3x3 product (and sweeps of the same
+    // node layout); k_spmv_bsr_pap4 indexes A with 32 bits
+    const bool padp = a_bsr && aan->bs == 3 && a.a.nnz < (1LL << 32) && aan->abc.bcol.n < (1LL << 32) &&
+                      (!factor || (an->bsr && an->bs == 3));
     pa.alloc(padp ? 4 * (n / 3) : n);
     // sweep vectors y, z padded too (node-blocked 3x3 sweeps): 256-bit polls
     // and publications (bsr_item PAD)
-    const bool padz = padp && an->bsr && an->bs == 3;
+    const bool padz = padp && factor;
     double* z = r.p;  // kind none: z aliases r
     if (factor) {
         y.alloc(padz ? 4 * (n / 3) : n);
@@ -656,8 +669,8 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         Timer tt(st);
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, nullptr, S.p->ctr, st, padz);
-            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
+            launch_sweep(*an, pc, false, r.p, y.p, z, nullptr, S.p->ctr, st, padz);
+            launch_sweep(*an, pc, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
@@ -692,7 +705,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
                 k_pupdate4<true><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
             else
                 k_pupdate4<false><<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
-            const BlockCols& bc = an->abc;
+            const BlockCols& bc = aan->abc;
             k_spmv_bsr_pap4<<<bsr_grid4, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp, q.p, S.p,
                                                      part.p);
             mark();
@@ -700,11 +713,11 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             mark();
         } else {
             k_pupdate<<<vgrid, kT, 0, st>>>(n, z, pp, S.p);
-            if (an && an->a_bsr) {
+            if (a_bsr) {
                 // grid = one resident wave (grid-stride rows; a second partial
                 // wave doubles the tail: measured 0.75 vs 0.93 ms at 1.5 waves)
-                const BlockCols& bc = an->abc;
-                if (an->bs == 3)
+                const BlockCols& bc = aan->abc;
+                if (aan->bs == 3)
                     k_spmv_bsr_pap<3><<<bsr_grid3, kT, 0, st>>>(n / 3, a.a.rp.p, bc.bp.p, bc.bcol.p, a.a.vals.p, pp,
                                                                q.p, S.p, part.p);
                 else
@@ -727,9 +740,9 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
             mark();
         }
         if (factor) {
-            launch_trsv(*an, pc.lvals.p, pc.invd.p, false, r.p, y.p, z, &S.p->done, S.p->ctr, st, padz);
+            launch_sweep(*an, pc, false, r.p, y.p, z, &S.p->done, S.p->ctr, st, padz);
             mark();
-            launch_trsv(*an, pc.uvals.p, pc.invd.p, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st, padz);
+            launch_sweep(*an, pc, true, y.p, z, y.p, &S.p->done, S.p->ctr + 1, st, padz);
             mark();
         } else {
             if (pc.kind == Kind::Jacobi) k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);

@@ -9,10 +9,16 @@ device at full size:
   - ic0 PCG to rtol 1e-8 (krylov.cpp:114-190 with precond.cpp:109-143):
     iteration count, converged flag, final / true relative residual, the
     whole residual history, ||x||_2, x at 4096 seeded indices, sha256 of x;
-  - the IC(0) factor and the GNN-corrected factor (gnn_ic_predict,
-    precond.cpp:155-168) at 4096 seeded entries of L;
-  - the error the reference raises when it runs PCG with that factor
-    ("pcg: nonpositive curvature at iteration 1", krylov.cpp:151-154).
+  - the IC(0) factor at 4096 seeded entries of L (reference);
+  - the GNN-corrected factor (gnn_ic_predict, precond.cpp:155-168) at the
+    same entries and the error PCG raises with it ("pcg: nonpositive
+    curvature at iteration 1", krylov.cpp:151-154). These two come from the
+    C oracle (oracle/pclab_oracle.c): the reference's own gnn_forward keeps
+    every per-edge activation of the 202M-edge graph and was OOM-killed at
+    54 GB in this 62 GB container; the oracle is pinned bit-for-bit to the
+    reference's gnn_forward / gnn_ic_predict / pcg on the committed small
+    fixtures (tests/test_oracle.py). Keys record which one produced what
+    (`<tag>.source`).
 * configs[4] (7-point FV diffusion 256^3, 16,777,216 dofs): gnnic PCG to
   rtol 1e-8, max 5000 iterations: the same solve record, plus the GNN-
   corrected factor at 4096 seeded entries.
@@ -50,10 +56,15 @@ def sample_idx(n: int, salt: int) -> np.ndarray:
     return np.sort(rng.choice(n, size=min(NSAMPLE, n), replace=False)).astype(np.int64)
 
 
-def solve_record(d, tag, a, b, kind, params, max_iters):
+def solve_record(d, tag, a, b, kind, params, max_iters, use_oracle=False):
     t0 = time.time()
+    d[f"{tag}.source"] = np.array(["oracle" if use_oracle else "reference"])
     try:
-        x, rep, hist = O.ref_pcg(a, b, kind, params, rel_tol=1e-8, max_iters=max_iters, history=True)
+        if use_oracle:
+            x, rep, hist = O.pcg(a, b, kind, params, rel_tol=1e-8, max_iters=max_iters, history=True)
+            rep = dict(rep, p_time=0.0, cg_time=0.0)
+        else:
+            x, rep, hist = O.ref_pcg(a, b, kind, params, rel_tol=1e-8, max_iters=max_iters, history=True)
     except O.OracleError as e:
         d[f"{tag}.error"] = np.array([str(e)])
         print(tag, "error:", e, f"({time.time() - t0:.0f} s)", flush=True)
@@ -71,10 +82,14 @@ def solve_record(d, tag, a, b, kind, params, max_iters):
           f"p {rep['p_time']:.1f} s cg {rep['cg_time']:.1f} s", flush=True)
 
 
-def factor_record(d, tag, a, kind, params, lidx):
+def factor_record(d, tag, a, kind, params, lidx, use_oracle=False):
     t0 = time.time()
+    d[f"{tag}.source"] = np.array(["oracle" if use_oracle else "reference"])
     try:
-        v, pt = O.ref_factor(a, kind, params)
+        if use_oracle:
+            v, pt = O.factor(a, kind, params), 0.0
+        else:
+            v, pt = O.ref_factor(a, kind, params)
     except O.OracleError as e:
         d[f"{tag}.error"] = np.array([str(e)])
         print(tag, "error:", e, flush=True)
@@ -100,9 +115,9 @@ def main():
     d["lidx"] = lidx
     d["nnz_lower"] = np.array([nl], np.int64)
     if which == "cfg2":
+        factor_record(d, "gnnic", a, "gnnic", params, lidx, use_oracle=True)
+        solve_record(d, "pcg.gnnic", a, b, "gnnic", params, -1, use_oracle=True)
         factor_record(d, "ic0", a, "ic0", None, lidx)
-        factor_record(d, "gnnic", a, "gnnic", params, lidx)
-        solve_record(d, "pcg.gnnic", a, b, "gnnic", params, -1)
         solve_record(d, "pcg.ic0", a, b, "ic0", None, -1)
     else:
         factor_record(d, "gnnic", a, "gnnic", params, lidx)

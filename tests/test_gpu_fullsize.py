@@ -2,6 +2,8 @@
 assembly, level sets and the IC(0) factor bit-exact against the oracle at
 5.01M dofs; the first PCG iterations track the oracle's residual history;
 the GNN-corrected factor at 202k dofs within 1e-5 relative."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -95,20 +97,89 @@ def test_config4_scaled_gnnic_converges_like_oracle():
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
 
 
-def test_config4_fullsize_gnnic_converges_and_is_deterministic():
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden(which):
+    path = os.path.join(GOLD, f"fullsize_{which}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing committed golden {path} (tests/golden/make_fullsize.py)")
+    return np.load(path)
+
+
+def sample_rel(got, ref):
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)))
+
+
+def test_config4_fullsize_gnnic_against_reference():
     """configs[4] at full size (256^3 FV diffusion, 16.8M unknowns, 10^6
-    conductivity contrast): the GNN-corrected IC(0) PCG reaches rel 1e-8
-    within the 5000-iteration cap, the true residual ||b - Ax|| / ||b||
-    agrees with the recurrence, and a second solve is bit-identical (the
-    oracle cannot run at this size; the 40^3 test above holds the oracle
-    parity for this family)."""
+    conductivity contrast) against the reference's own run
+    (tests/golden/fullsize_cfg4.npz, make_fullsize.py): GNN-corrected factor
+    within 1e-5 relative at 4096 seeded entries; PCG (gnnic, rtol 1e-8,
+    max 5000) converged, x within 1e-8 relative at 4096 seeded indices and
+    in norm, true residual <= 1e-8 like the reference's. The iteration count
+    is held to 1% of the reference's 1335: near the end the reference's own
+    residual decays only ~1.6% per iteration on average and not
+    monotonically (1.09e-8 -> 1.17e-8 within four iterations of its
+    history), so dot products summed in a different order (the reference
+    adds 16.8M products sequentially) cross 1e-8 a few iterations apart
+    while the solutions agree to ~6e-10. A second solve is bit-identical."""
     import hashlib
+    g = golden("cfg4")
     w = P.workloads.CONFIGS[4]
     a, b, model = P.workloads.build(w)
-    assert a.n == 256 ** 3
+    assert a.n == int(g["n"][0]) == 256 ** 3 and a.nnz == int(g["n"][1])
+    pc = P.Precond(a, "gnnic", model)
+    f = pc.factor()
+    assert len(f) == int(g["nnz_lower"][0])
+    assert sample_rel(f[g["lidx"]], g["gnnic.vals"]) < 1e-5
+    del f, pc
     x1, r1 = P.pcg_solve(a, b, "gnnic", model, rel_tol=w.rel_tol, max_iters=w.max_iters)
-    assert r1["converged"] and r1["iterations"] < w.max_iters
-    assert r1["true_rel_residual"] <= 2e-8
+    its_ref, conv_ref = (int(v) for v in g["pcg.gnnic.iters"])
+    assert conv_ref and r1["converged"]
+    assert abs(r1["iterations"] - its_ref) <= 0.01 * its_ref
+    xi, xr = g["pcg.gnnic.xidx"], g["pcg.gnnic.x"]
+    assert np.linalg.norm(x1[xi] - xr) <= 1e-8 * np.linalg.norm(xr)
+    assert abs(np.linalg.norm(x1) - g["pcg.gnnic.xnorm"][0]) <= 1e-8 * g["pcg.gnnic.xnorm"][0]
+    assert r1["true_rel_residual"] <= 1.01e-8 and g["pcg.gnnic.resid"][1] <= 1.01e-8
     x2, r2 = P.pcg_solve(a, b, "gnnic", model, rel_tol=w.rel_tol, max_iters=w.max_iters)
     assert r2["iterations"] == r1["iterations"]
     assert hashlib.sha256(x1.tobytes()).digest() == hashlib.sha256(x2.tobytes()).digest()
+
+
+def test_config2_fullsize_against_reference():
+    """configs[2] (the headline, 5,012,994 dofs) against the reference's run
+    (tests/golden/fullsize_cfg2.npz): IC(0) factor bit-exact at 4096 seeded
+    entries; the full ic0 PCG to rtol 1e-8 within +-1 iteration of the
+    reference, x within 1e-8 relative at 4096 seeded indices and in norm;
+    the GNN-corrected factor within 1e-5 relative; and PCG with it fails
+    exactly like the reference's (precond.cpp:155-168 adds the random-init
+    network output unscaled; krylov.cpp:151-154 raises)."""
+    g = golden("cfg2")
+    w = P.workloads.CONFIGS[2]
+    a, b, model = P.workloads.build(w)
+    assert a.n == int(g["n"][0]) and a.nnz == int(g["n"][1])
+    lidx = g["lidx"]
+    ic = P.Precond(a, "ic0")
+    assert np.array_equal(bits(ic.factor()[lidx]), bits(g["ic0.vals"]))
+    bt = torch.from_numpy(b).cuda()
+    xt = torch.zeros_like(bt)
+    rep = ic.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=w.rel_tol, max_iters=w.max_iters,
+                          record_history=True)
+    its_ref, conv_ref = (int(v) for v in g["pcg.ic0.iters"])
+    assert conv_ref and rep["converged"]
+    assert abs(rep["iterations"] - its_ref) <= 1
+    x = xt.cpu().numpy()
+    xi, xr = g["pcg.ic0.xidx"], g["pcg.ic0.x"]
+    assert np.linalg.norm(x[xi] - xr) <= 1e-8 * np.linalg.norm(xr)
+    assert abs(np.linalg.norm(x) - g["pcg.ic0.xnorm"][0]) <= 1e-8 * g["pcg.ic0.xnorm"][0]
+    h, hr = np.array(rep["residual_history"]), g["pcg.ic0.hist"]
+    m = min(len(h), len(hr))
+    assert np.max(np.abs(h[:50] - hr[:50]) / hr[:50]) < 1e-8  # early iterates agree to rounding
+    del ic
+    gn = P.Precond(a, "gnnic", model)
+    assert sample_rel(gn.factor()[lidx], g["gnnic.vals"]) < 1e-5
+    with pytest.raises(P.NumericError) as e:
+        gn.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=w.rel_tol, max_iters=w.max_iters)
+    assert str(e.value) == str(g["pcg.gnnic.error"][0])
+    assert m > 0
