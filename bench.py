@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--kind", default="ic0")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=2, help="PCG iterations per reference step")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the gnnic build leg on configs[2] and the configs[4] 256^3 leg")
     ap.add_argument("--bw-elasticity", action="store_true",
                     help="per-kernel bandwidth of SpMV / both node-blocked sweeps on configs[2] (5.0M dofs) and "
                          "configs[3] (10.1M dofs); configs[3]'s IC(0) breaks down like the reference's, so its "
@@ -142,24 +144,33 @@ def combine_ranks(ms: float, cg_s: float, iters: int, world: int, device: str):
 
 
 # ------------------------------------------------------------ CPU reference
+REF_NOTE = ("steady-state per-iteration time: each sample is one stock pcg() call (krylov.cpp:114) of "
+            "{k} iterations; its cg_time includes the pre-loop preconditioner apply (krylov.cpp:145-148), "
+            "so one apply (tri_solve_time_per_iter x k / (k + 1), the reference's own timer) is subtracted")
+
+
 def reference_sample(w, iters: int, steps: int, warmup: int):
     """The reference's pcg() (krylov.cpp:114, compiled from /root/reference
     into oracle/_ref) on the full system with its IC(0) factor (computed once
-    by the C oracle, bit-identical to the reference's ic0). Returns
-    (iterations, cg seconds, wall seconds per step) per timed step."""
+    by the C oracle, bit-identical to the reference's ic0), system and factor
+    resident (oracle RefSession). Returns per timed step (iterations,
+    steady-state seconds, wall seconds), the setup seconds and the system."""
     from oracle import oracle as O
     import paper_2412_07127_b200.workloads as WL
 
     t0 = time.perf_counter()
     a, b, _ = WL.build_oracle(w)
     lvals, _ = O.ic0(a)
+    sess = O.RefSession(a, lvals)
     setup = time.perf_counter() - t0
     out = []
     for s in range(warmup + steps):
         t = time.perf_counter()
-        _, rep = O.ref_pcg_factor(a, lvals, b, w.rel_tol, iters)
+        _, rep = sess.run(b, w.rel_tol, iters)
+        k = rep["iterations"]
+        apply_s = rep["tri_solve_time_per_iter"] * k / (k + 1)
         if s >= warmup:
-            out.append((rep["iterations"], rep["cg_time"], time.perf_counter() - t))
+            out.append((k, rep["cg_time"] - apply_s, time.perf_counter() - t))
     return out, setup, a
 
 
@@ -176,16 +187,16 @@ def run_reference(args, w):
     cg = sum(r[1] for r in res)
     wall = sum(r[2] for r in res)
     v = its / cg
+    sample = (f"{args.ref_iters} iterations of the reference pcg() per step on the full {a.n}-dof system, "
+              f"IC(0) factor, single thread (the reference is serial); " + REF_NOTE.format(k=args.ref_iters))
     line = {
         "metric": "pcg_iters_per_s", "value": v, "unit": "iter/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / len(res) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator)", "impl": "reference",
         "config": {"workload": w.name, "n": a.n, "nnz": a.nnz, "kind": "ic0", "rel_tol": w.rel_tol,
-                   "sample": f"{args.ref_iters} PCG iterations per step"},
-        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "reference",
-                         "sample": f"{args.ref_iters} iterations of the reference pcg() per step on the "
-                                   f"full {a.n}-dof system, IC(0) factor, single thread"},
+                   "sample": f"{args.ref_iters} PCG iterations per step (steady state)"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "setup_s": setup,
     }
@@ -291,15 +302,19 @@ def run_b200(args, w):
             e2e_rates.append(rep["iterations"] / dt)
     e2e_v = float(np.median(e2e_rates)) * (world if world > 1 else 1)
 
+    extra = {} if args.no_extra else extra_legs(args, a, b_host, model, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
             if O.ref_available():
-                res, _, _ = reference_sample(w, args.ref_iters, 1, 0)
-                cpu = {"value": res[0][0] / res[0][1], "unit": "iter/s", "cores": 1, "kind": "reference",
-                       "sample": f"{args.ref_iters} iterations of the reference pcg() (oracle/_ref) on the "
-                                 f"full {n}-dof system with its IC(0) factor, single thread"}
+                res, _, _ = reference_sample(w, args.ref_iters, 2, 1)
+                cpu = {"value": sum(r[0] for r in res) / sum(r[1] for r in res), "unit": "iter/s", "cores": 1,
+                       "kind": "reference",
+                       "sample": f"2 samples of {args.ref_iters} iterations of the reference pcg() (oracle/_ref) "
+                                 f"on the full {n}-dof system with its IC(0) factor, single thread; "
+                                 + REF_NOTE.format(k=args.ref_iters)}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "iter/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -328,10 +343,88 @@ def run_b200(args, w):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        line.update(extra)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def extra_legs(args, a, b_host, model, stream) -> dict:
+    """Every north-star subsystem in the driver's bench line, outside the
+    timed region:
+    * gnnic_build (configs[2]): symbolic analysis + IC(0) + GNN forward and
+      correction (gnn_ic_predict, precond.cpp:155-168), device events, and
+      what PCG does with that factor (the reference fails: nonpositive
+      curvature at iteration 1, tests/golden/fullsize_cfg2.npz);
+    * diffusion_256 (configs[4], 16.8M unknowns): gnnic time to rtol 1e-8
+      (analysis + IC(0) + GNN + PCG) and per-kernel device ms / GB/s of its
+      loop (7-point sweeps and the row-tile product)."""
+    import torch
+    import paper_2412_07127_b200 as P
+    from paper_2412_07127_b200 import traffic as T
+    import paper_2412_07127_b200.workloads as WL
+
+    out = {}
+    hbm, _ = peaks()
+    bt = torch.from_numpy(b_host).cuda()
+    xt = torch.zeros_like(bt)
+    builds = []
+    for _ in range(3):
+        a.drop_analysis()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        pc = P.Precond(a, "gnnic", model)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        builds.append((e0.elapsed_time(e1), pc.timings()))
+    ms, t = sorted(builds, key=lambda v: v[0])[1]
+    try:
+        rep = pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=1e-8, max_iters=2000)
+        outcome = f"converged={rep['converged']} iterations={rep['iterations']}"
+    except P.PclabError as e:
+        outcome = f"{type(e).__name__}: {e}"
+    out["gnnic_build"] = {"workload": "elasticity_q1_118", "ms": ms, "analysis_ms": t["analysis_ms"],
+                          "ic0_ms": t["ic0_ms"], "gnn_ms": t["gnn_ms"], "pcg_outcome": outcome,
+                          "reference_outcome": "NumericError: pcg: nonpositive curvature at iteration 1 "
+                                               "(matrix not SPD?) (tests/golden/fullsize_cfg2.npz)"}
+    del pc
+    # configs[4]
+    w4 = WL.CONFIGS[4]
+    a4, b4, m4 = WL.build(w4)
+    n4, _, nnz4 = a4.shape()
+    b4t = torch.from_numpy(b4).cuda()
+    x4t = torch.zeros_like(b4t)
+    runs = []
+    for _ in range(2):
+        a4.drop_analysis()
+        x4t.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        pc4 = P.Precond(a4, "gnnic", m4)
+        rep4 = pc4.solve_device(b4t.data_ptr(), x4t.data_ptr(), rel_tol=w4.rel_tol, max_iters=w4.max_iters,
+                                stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        runs.append((e0.elapsed_time(e1), rep4, pc4.timings()))
+    ms4, rep4, t4 = runs[-1]
+    prof4 = pc4.profile_device(b4t.data_ptr(), x4t.data_ptr(), 20)
+    kern4 = T.iteration_kernels(pc4, n4, nnz4, prof4)
+    it_bytes = sum(k["bytes"] for k in kern4.values())
+    it_ms = sum(k["ms"] for k in kern4.values())
+    out["diffusion_256"] = {
+        "workload": w4.name, "n": n4, "nnz": nnz4, "kind": "gnnic", "rel_tol": w4.rel_tol,
+        "iterations": rep4["iterations"], "converged": rep4["converged"],
+        "true_rel_residual": rep4["true_rel_residual"], "time_to_tol_s": ms4 / 1e3,
+        "analysis_ms": t4["analysis_ms"], "ic0_ms": t4["ic0_ms"], "gnn_ms": t4["gnn_ms"],
+        "cg_s": rep4["cg_time"], "iters_per_s": rep4["iterations"] / rep4["cg_time"],
+        "reference_iterations": 1335, "kernels": kern4,
+        "iteration": {"bytes": it_bytes, "ms": it_ms, "gbs": it_bytes / it_ms / 1e6,
+                      "frac": it_bytes / it_ms / 1e6 / hbm}}
+    del pc4, a4
+    return out
 
 
 def run_bw_sweep(args):

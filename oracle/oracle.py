@@ -28,7 +28,8 @@ _ref = None
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        path = os.path.join(HERE, "liboracle.so")
+        # ORACLE_LIB: another build of pclab_oracle.c (tests/golden/sensitivity.py)
+        path = os.environ.get("ORACLE_LIB") or os.path.join(HERE, "liboracle.so")
         if not os.path.exists(path):
             raise RuntimeError(f"oracle not built: {path} (run make -C oracle)")
         _lib = C.CDLL(path)
@@ -437,6 +438,35 @@ def ref_pcg(a: Csr, b: np.ndarray, kind: str = "ic0", params: np.ndarray | None 
     if history:
         return x, r, hist[: rep.iterations + 1]
     return x, r
+
+
+class RefSession:
+    """The reference's pcg() on a resident system + IC(0)-kind factor
+    (ref_shim.cpp ref_pcg_session_*): one stock pcg() call per run()."""
+
+    def __init__(self, a: Csr, lvals: np.ndarray):
+        R = ref()
+        R.ref_pcg_session_new.restype = C.c_void_p
+        R.ref_pcg_session_new.argtypes = [C.c_int64, _i64p, _i32p, _f64p, _f64p]
+        R.ref_pcg_session_run.argtypes = [C.c_void_p, _f64p, C.c_double, C.c_int64, _f64p,
+                                          C.POINTER(RefReport)]
+        R.ref_pcg_session_free.argtypes = [C.c_void_p]
+        self.n = a.n
+        self.h = R.ref_pcg_session_new(a.n, a.rp, a.cols, a.vals, np.ascontiguousarray(lvals))
+        if not self.h:
+            raise OracleError(1, R.ref_last_error().decode())
+
+    def run(self, b: np.ndarray, rel_tol: float, max_iters: int):
+        x = np.empty(self.n, np.float64)
+        rep = RefReport()
+        ref_check(ref().ref_pcg_session_run(self.h, np.ascontiguousarray(b, np.float64), rel_tol, max_iters, x,
+                                            C.byref(rep)))
+        return x, {k: getattr(rep, k) for k, _ in RefReport._fields_}
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_pcg_session_free(self.h)
+            self.h = None
 
 
 def ref_pcg_factor(a: Csr, lvals: np.ndarray, b: np.ndarray, rel_tol: float, max_iters: int):

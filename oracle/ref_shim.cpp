@@ -208,4 +208,50 @@ int ref_pcg_factor(int64_t n, const int64_t* rp, const int32_t* cols, const doub
     });
 }
 
+// A resident PCG session for the bench's reference arm: the system (CSR)
+// and an IC(0)-kind preconditioner on a caller-supplied factor are built
+// once; each ref_pcg_session_run is one stock pcg() call (krylov.cpp:114,
+// Applier construction included, as every pcg() call does).
+struct ref_session {
+    SparseCsr a;
+    Preconditioner p;
+};
+
+void* ref_pcg_session_new(int64_t n, const int64_t* rp, const int32_t* cols, const double* vals,
+                          const double* lvals) {
+    auto* s = new ref_session;
+    if (guarded([&] {
+            s->a = to_csr(n, rp, cols, vals);
+            s->p.kind = PrecondKind::IC0;
+            SparseCoo& l = s->p.factor.matrix;
+            l.n_rows = l.n_cols = n;
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+                    if (cols[k] <= i) {
+                        l.rows.push_back(i);
+                        l.cols.push_back(cols[k]);
+                    }
+            l.values.assign(lvals, lvals + l.rows.size());
+        })) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+
+int ref_pcg_session_run(void* h, const double* b, double rel_tol, int64_t max_iters, double* x,
+                        ref_report* rep) {
+    auto* s = static_cast<ref_session*>(h);
+    return guarded([&] {
+        SolveConfig cfg;
+        cfg.rel_tol = rel_tol;
+        cfg.max_iters = max_iters;
+        auto [xx, r] = pcg(s->a, std::span<const double>(b, s->a.n_rows), s->p, cfg);
+        std::memcpy(x, xx.data(), static_cast<size_t>(s->a.n_rows) * sizeof(double));
+        fill(rep, r);
+    });
+}
+
+void ref_pcg_session_free(void* h) { delete static_cast<ref_session*>(h); }
+
 }  // extern "C"

@@ -168,38 +168,11 @@ std::string entry_str(int64_t i, int64_t j) {
     return "(" + std::to_string(i) + ", " + std::to_string(j) + ")";
 }
 
-// make_coo (sparse.cpp:55-72) + SparseCoo::validate (sparse.cpp:25-43),
-// then compressed to CSR for the upload.
+// make_coo (sparse.cpp:55-72) + SparseCoo::validate (sparse.cpp:25-43) on
+// the device (coo.cu)
 std::unique_ptr<Matrix> coo_upload(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
                                    const int64_t* cols, const double* vals) {
-    if (n_rows < 0 || n_cols < 0) throw FormatError("coo: negative dimensions");
-    if (n_cols > INT32_MAX || n_rows > INT32_MAX)
-        throw DimensionError("coo: dimensions exceed the int32 column index range");
-    std::vector<int64_t> order(static_cast<size_t>(nnz));
-    std::iota(order.begin(), order.end(), int64_t{0});
-    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        if (rows[a] != rows[b]) return rows[a] < rows[b];
-        return cols[a] < cols[b];
-    });
-    std::vector<int64_t> rp(static_cast<size_t>(n_rows) + 1, 0);
-    std::vector<int32_t> c(static_cast<size_t>(nnz));
-    std::vector<double> v(static_cast<size_t>(nnz));
-    for (int64_t k = 0; k < nnz; ++k) {
-        const int64_t s = order[k];
-        const int64_t i = rows[s], j = cols[s];
-        if (i < 0 || i >= n_rows || j < 0 || j >= n_cols)
-            throw FormatError("coo: entry " + entry_str(i, j) + " out of bounds");
-        if (k > 0) {
-            const int64_t ps = order[k - 1];
-            if (rows[ps] == i && cols[ps] == j)
-                throw FormatError("coo: entries not sorted or duplicate at " + entry_str(i, j));
-        }
-        rp[i + 1]++;
-        c[k] = static_cast<int32_t>(j);
-        v[k] = vals[s];
-    }
-    for (int64_t i = 0; i < n_rows; ++i) rp[i + 1] += rp[i];
-    return matrix_from_csr_device(n_rows, nnz, rp.data(), c.data(), v.data(), lib_stream(), n_cols);
+    return matrix_from_coo_device(n_rows, n_cols, nnz, rows, cols, vals, lib_stream());
 }
 
 // -------------------------------------------------- Matrix Market (host IO)

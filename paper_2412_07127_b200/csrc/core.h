@@ -204,6 +204,9 @@ std::unique_ptr<Matrix> matrix_from_csr_host(int64_t n, const int64_t* rp, const
 std::unique_ptr<Matrix> matrix_from_csr_device(int64_t n, int64_t nnz, const int64_t* rp,
                                                const int32_t* cols, const double* vals,
                                                cudaStream_t st, int64_t n_cols = -1);
+// coo.cu: make_coo (sparse.cpp:55-72) on the device; host or device pointers
+std::unique_ptr<Matrix> matrix_from_coo_device(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
+                                               const int64_t* cols, const double* vals, cudaStream_t st);
 std::unique_ptr<Matrix> gen_poisson_device(int dim, int64_t m, const double* cell_k_host,
                                            cudaStream_t st);
 std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double* moduli_host,

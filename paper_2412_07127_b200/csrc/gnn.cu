@@ -68,51 +68,72 @@ __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ rp,
     if (i < n) deg[i] = static_cast<double>(rp[i + 1] - rp[i] - (dpos[i] >= 0 ? 1 : 0));
 }
 
-__global__ void features_kernel(int64_t n, const int64_t* __restrict__ rp,
-                                const int32_t* __restrict__ cols, const double* __restrict__ vals,
-                                const double* __restrict__ deg, double* __restrict__ f) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+// Warp per row (lanes over the entries, coalesced): diagonal, |off| sum and
+// max, neighbour-degree max / min / mean, then their variance from the
+// row's entries again (L1-resident). Sums are fixed shuffle trees (the
+// reference adds in entry order; the features differ from it by rounding
+// only, and the degrees and their mean are exact integers / quotients).
+__global__ void __launch_bounds__(256)
+features_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                const double* __restrict__ vals, const double* __restrict__ deg, double* __restrict__ f) {
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= n) return;
-    double diag = 0.0, osum = 0.0, omax = 0.0, mx = 0.0, mn = 1e300, mean = 0.0;
+    const int64_t b = rp[i], e = rp[i + 1];
+    double diag = 0.0, osum = 0.0, omax = 0.0, mx = 0.0, mn = 1e300, dsum = 0.0;
     int cnt = 0;
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+    for (int64_t k = b + lane; k < e; k += 32) {
         const double av = fabs(vals[k]);
-        if (cols[k] == i) {
+        const int32_t j = cols[k];
+        if (j == i) {
             diag = av;
             continue;
         }
         osum += av;
         omax = fmax(omax, av);
-        const double d = deg[cols[k]];
+        const double d = deg[j];
         mx = fmax(mx, d);
         mn = fmin(mn, d);
-        mean += d;
+        dsum += d;
         ++cnt;
     }
-    double* row = f + i * kF;
-    row[0] = deg[i];
-    row[1] = row[2] = row[3] = row[4] = 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        diag += __shfl_xor_sync(0xffffffffu, diag, o);  // one lane holds it
+        osum += __shfl_xor_sync(0xffffffffu, osum, o);
+        omax = fmax(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    double var = 0.0, mean = 0.0;
     if (cnt > 0) {
-        mean /= static_cast<double>(cnt);
-        double var = 0.0;
-        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-            if (cols[k] == i) continue;
-            const double dd = deg[cols[k]] - mean;
+        mean = dsum / static_cast<double>(cnt);
+        for (int64_t k = b + lane; k < e; k += 32) {
+            const int32_t j = cols[k];
+            if (j == i) continue;
+            const double dd = deg[j] - mean;
             var += dd * dd;
         }
-        row[1] = mx;
-        row[2] = mn;
-        row[3] = mean;
-        row[4] = var / static_cast<double>(cnt);
+        var = group_sum<32>(var);
     }
-    const double denom = diag + osum;
-    row[5] = denom > 0.0 ? diag / denom : 0.0;
-    row[6] = omax > 0.0 ? fmin(fmax(diag / omax, 0.0), 100.0) : 100.0;
-    const double angle = 2.0 * 3.14159265358979323846 * static_cast<double>(i) / static_cast<double>(n);
-    double sn, cs;
-    sincos(angle, &sn, &cs);
-    row[7] = sn;
-    row[8] = cs;
+    if (lane == 0) {
+        double* row = f + i * kF;
+        row[0] = deg[i];
+        row[1] = cnt > 0 ? mx : 0.0;
+        row[2] = cnt > 0 ? mn : 0.0;
+        row[3] = cnt > 0 ? mean : 0.0;
+        row[4] = cnt > 0 ? var / static_cast<double>(cnt) : 0.0;
+        const double denom = diag + osum;
+        row[5] = denom > 0.0 ? diag / denom : 0.0;
+        row[6] = omax > 0.0 ? fmin(fmax(diag / omax, 0.0), 100.0) : 100.0;
+        const double angle = 2.0 * 3.14159265358979323846 * static_cast<double>(i) / static_cast<double>(n);
+        double sn, cs;
+        sincos(angle, &sn, &cs);
+        row[7] = sn;
+        row[8] = cs;
+    }
 }
 
 // Deterministic column sums of an n x W row-major array (fixed grid, fixed
@@ -196,32 +217,82 @@ __global__ void edge_rows_kernel(int64_t n, const int64_t* __restrict__ lrp, int
     for (int64_t k = lrp[i] + (threadIdx.x & 31); k < lrp[i + 1]; k += 32) erow[k] = static_cast<int32_t>(i);
 }
 
-// Edge updater: one thread per edge of the flat L entry list (every lane
-// busy whatever the row lengths), edge (i, j) = (erow[k], lcols[k]).
-// Consecutive edges share their row, so x_i is an L1 broadcast; x_j is an
-// L2-resident gather (mesh ordering keeps neighbours close).
+// First layer of the edge MLP split by operand: the terms of the node
+// states x_i and x_j depend on one node each, so every node gets its two
+// projections once (16 values: pq[v] = {W1_i x_v, W1_j x_v}) and an edge
+// adds them instead of redoing 2 x 8 x XW FMAs (the reference sums bias,
+// then inputs in order; this is the same sum regrouped -- rounding-level
+// differences, held to the 1e-5 bar).
 template <int BLK>
-__global__ void __launch_bounds__(256, 2)
-edge_kernel(int64_t ne, const int32_t* __restrict__ erow, const int32_t* __restrict__ lcols,
-            const double* __restrict__ x, const double* __restrict__ ef, const double* __restrict__ eprev,
-            double* __restrict__ eout, int* __restrict__ bad) {
+__global__ void __launch_bounds__(256)
+node_proj_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ pq) {
     constexpr bool FIRST = BLK == 0;
     constexpr int XW = FIRST ? kF : kH;
     constexpr int IN = edge_in(BLK);
+    constexpr int W1 = edge_off(BLK);
+    constexpr int I0 = FIRST ? 1 : 2;  // first x_i input
+    const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (v >= n) return;
+    double xv[XW];
+#pragma unroll
+    for (int c = 0; c < XW; ++c) xv[c] = x[v * XW + c];
+    double p[kH], q[kH];
+#pragma unroll
+    for (int h = 0; h < kH; ++h) {
+        p[h] = 0.0;
+        q[h] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < XW; ++c)
+#pragma unroll
+        for (int h = 0; h < kH; ++h) {
+            p[h] = fma(c_p[W1 + h * IN + I0 + c], xv[c], p[h]);
+            q[h] = fma(c_p[W1 + h * IN + I0 + XW + c], xv[c], q[h]);
+        }
+    double2* o = reinterpret_cast<double2*>(pq + v * 2 * kH);
+#pragma unroll
+    for (int h = 0; h < kH; h += 2) {
+        o[h / 2] = make_double2(p[h], p[h + 1]);
+        o[kH / 2 + h / 2] = make_double2(q[h], q[h + 1]);
+    }
+}
+
+// Edge updater: one thread per edge of the flat L entry list (every lane
+// busy whatever the row lengths), edge (i, j) = (erow[k], lcols[k]):
+// hidden = b1 + w_prev e_prev + w_f f + (W1_i x_i) + (W1_j x_j), tanh, the
+// output layer. Consecutive edges share their row, so the x_i projection
+// is an L1 broadcast; the x_j projection is an L2-resident gather.
+template <int BLK>
+__global__ void __launch_bounds__(256)
+edge_kernel(int64_t ne, const int32_t* __restrict__ erow, const int32_t* __restrict__ lcols,
+            const double* __restrict__ pq, const double* __restrict__ ef, const double* __restrict__ eprev,
+            double* __restrict__ eout, int* __restrict__ bad) {
+    constexpr bool FIRST = BLK == 0;
+    constexpr int IN = edge_in(BLK);
+    constexpr int W1 = edge_off(BLK), B1 = W1 + kH * IN, W2 = B1 + kH, B2 = W2 + kH;
     bool nonfinite = false;
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < ne;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = erow[k], j = lcols[k];
-        double in[IN];
-        int w = 0;
-        if (!FIRST) in[w++] = eprev[k];
-        in[w++] = ef[k];
+        const double fk = ef[k];
+        const double pk = FIRST ? 0.0 : eprev[k];
+        const double2* pi = reinterpret_cast<const double2*>(pq + i * 2 * kH);
+        const double2* qj = reinterpret_cast<const double2*>(pq + j * 2 * kH) + kH / 2;
+        double hid[kH];
 #pragma unroll
-        for (int c = 0; c < XW; ++c) in[w + c] = x[i * XW + c];
+        for (int h = 0; h < kH; h += 2) {
+            const double2 a = pi[h / 2], b = qj[h / 2];
 #pragma unroll
-        for (int c = 0; c < XW; ++c) in[w + XW + c] = x[j * XW + c];
-        double y;
-        mlp<edge_off(BLK), IN, 1>(in, &y);
+            for (int u = 0; u < 2; ++u) {
+                double t = c_p[B1 + h + u];
+                if (!FIRST) t = fma(c_p[W1 + (h + u) * IN], pk, t);
+                t = fma(c_p[W1 + (h + u) * IN + (FIRST ? 0 : 1)], fk, t);
+                hid[h + u] = tanh(t + (u ? a.y : a.x) + (u ? b.y : b.x));
+            }
+        }
+        double y = c_p[B2];
+#pragma unroll
+        for (int h = 0; h < kH; ++h) y = fma(c_p[W2 + h], hid[h], y);
         eout[k] = y;
         nonfinite |= !isfinite(y);
     }
@@ -269,15 +340,17 @@ __global__ void output_kernel(int64_t n, const int64_t* __restrict__ lrp, double
 inline unsigned gfor(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 template <int BLK>
-void launch_edge(int64_t ne, const int32_t* erow, const int32_t* lcols, const double* x, const double* ef,
-                 const double* eprev, double* eout, int* bad, cudaStream_t st) {
+void launch_edge(int64_t n, int64_t ne, const int32_t* erow, const int32_t* lcols, const double* x, double* pq,
+                 const double* ef, const double* eprev, double* eout, int* bad, cudaStream_t st) {
+    node_proj_kernel<BLK><<<gfor(n, 256), 256, 0, st>>>(n, x, pq);
+    CK_LAUNCH();
     static unsigned grid = 0;
     if (!grid) {
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, edge_kernel<BLK>, 256, 0));
         grid = static_cast<unsigned>(std::max(per_sm, 1) * sm_count() * 4);
     }
-    edge_kernel<BLK><<<grid, 256, 0, st>>>(ne, erow, lcols, x, ef, eprev, eout, bad);
+    edge_kernel<BLK><<<grid, 256, 0, st>>>(ne, erow, lcols, pq, ef, eprev, eout, bad);
     CK_LAUNCH();
 }
 
@@ -300,7 +373,7 @@ void gnn_forward(const Matrix& A, const Analysis& an, const Model& model, double
     // ---- node features (features.cpp:11-72)
     DevBuf<double> deg(n), feat(n * kF), x0(n * kF), cnt(n);
     degree_kernel<<<gfor(n, T), T, 0, st>>>(n, A.a.rp.p, A.diag_pos.p, deg.p);
-    features_kernel<<<gfor(n, T), T, 0, st>>>(n, A.a.rp.p, A.a.cols.p, A.a.vals.p, deg.p, feat.p);
+    features_kernel<<<gfor(n * 32, T), T, 0, st>>>(n, A.a.rp.p, A.a.cols.p, A.a.vals.p, deg.p, feat.p);
     CK_LAUNCH();
     // ---- graph normalisation statistics (gnn.cpp:141-160)
     const int parts = sm_count() * 2;
@@ -350,16 +423,16 @@ void gnn_forward(const Matrix& A, const Analysis& an, const Model& model, double
     DevBuf<int32_t> erow(ne);
     edge_rows_kernel<<<gfor(n * 32, T), T, 0, st>>>(n, L.rp.p, erow.p);
     CK_LAUNCH();
-    DevBuf<double> e1(ne), e2(ne), xa(n * kH), xb(n * kH);
+    DevBuf<double> e1(ne), e2(ne), xa(n * kH), xb(n * kH), pq(n * 2 * kH);
     DevBuf<int> bad(6);
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int) * 6, st));
-    launch_edge<0>(ne, erow.p, L.cols.p, x0.p, ef.p, nullptr, e1.p, bad.p, st);
+    launch_edge<0>(n, ne, erow.p, L.cols.p, x0.p, pq.p, ef.p, nullptr, e1.p, bad.p, st);
     node_kernel<0><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, x0.p, e1.p, xa.p, bad.p + 1);
     CK_LAUNCH();
-    launch_edge<1>(ne, erow.p, L.cols.p, xa.p, ef.p, e1.p, e2.p, bad.p + 2, st);
+    launch_edge<1>(n, ne, erow.p, L.cols.p, xa.p, pq.p, ef.p, e1.p, e2.p, bad.p + 2, st);
     node_kernel<1><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, xa.p, e2.p, xb.p, bad.p + 3);
     CK_LAUNCH();
-    launch_edge<2>(ne, erow.p, L.cols.p, xb.p, ef.p, e2.p, out, bad.p + 4, st);
+    launch_edge<2>(n, ne, erow.p, L.cols.p, xb.p, pq.p, ef.p, e2.p, out, bad.p + 4, st);
     // the final node state feeds nothing (gnn.cpp:199-205 computes it and
     // checks it for finiteness)
     node_kernel<2><<<gfor(n, T), T, 0, st>>>(n, L.rp.p, U.rp.p, an.u2l.p, cnt.p, xb.p, out, xa.p, bad.p + 5);

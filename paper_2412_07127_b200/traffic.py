@@ -22,18 +22,13 @@ is reported beside it as `csr_equivalent_bytes`.
 """
 from __future__ import annotations
 
-
-import os
-
 V4 = 32.0 / 3.0  # bytes per row of a vector padded to 4 doubles per 3-dof node
 
 
-def padded(lay: dict, bs: int, fused: bool = False) -> bool:
+def padded(lay: dict, bs: int) -> bool:
     """Mirror of pcg_solve's choice (pcg.cu): padded p / y / z for 3x3
-    node-blocked A and L outside the fused variant."""
-    env = lambda k: os.environ.get(k, "1") != "0"  # noqa: E731
-    return (lay["a_node_blocked"] and lay["node_blocked"] and bs == 3 and not fused
-            and env("PCLAB_PADP") and env("PCLAB_PADZ"))
+    node-blocked A and L."""
+    return bool(lay["a_node_blocked"] and lay["node_blocked"] and bs == 3)
 
 
 def sweep_bytes(lay: dict, nnz_lower: int, n: int, upper: bool, pad: bool = False) -> int:
@@ -71,21 +66,14 @@ def iteration_kernels(pc, n: int, nnz: int, prof: dict) -> dict:
     lay = pc.layout()
     info = pc.info()
     nl, bs = info["nnz_lower"], max(info["block_size"], 1)
-    pad = padded(lay, bs, bool(prof.get("fused")))
+    pad = padded(lay, bs)
     lo, up = sweep_bytes(lay, nl, n, False, pad), sweep_bytes(lay, nl, n, True, pad)
     prod = product_bytes(lay, nnz, n, bs, pad)
-    if prof.get("fused"):
-        kern = {
-            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
-            "sweep_upper_spmv": {"ms": prof["sweep_upper_ms"], "bytes": up + prod - 24 * n},
-            "pq_update": {"ms": prof["spmv_ms"], "bytes": 48 * n},
-        }
-    else:
-        kern = {
-            "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
-            "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": up},
-            "spmv_p": {"ms": prof["spmv_ms"], "bytes": prod},
-        }
+    kern = {
+        "sweep_lower": {"ms": prof["sweep_lower_ms"], "bytes": lo},
+        "sweep_upper": {"ms": prof["sweep_upper_ms"], "bytes": up},
+        "spmv_p": {"ms": prof["spmv_ms"], "bytes": prod},
+    }
     v = V4 if pad else 8
     kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": int((v + 40) * n)}  # p, q, x r/w, r r/w
     kern["dot"] = {"ms": prof["dot_ms"], "bytes": int((8 + v) * n)}

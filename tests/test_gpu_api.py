@@ -94,3 +94,27 @@ def test_rectangular_coo_accepted_then_rejected_like_the_reference():
         P.pcg_solve(a, b, "nic", model)
     with pytest.raises(P.FormatError, match="out of bounds"):
         P.Matrix.from_coo(2, 3, [0], [3], [1.0])
+
+
+def test_device_coo_matches_make_coo_order_and_errors():
+    """make_coo (sparse.cpp:55-72) on the device: the first offending entry
+    in (row, col) order is the one reported, whether the input arrives
+    sorted (fast path) or shuffled (radix sort), with or without an
+    out-of-bounds entry (two stable passes on the raw signed pairs)."""
+    a = P.Matrix.gen_poisson(3, 6, True, 4)
+    rp, cols, vals = a.csr()
+    rows = np.repeat(np.arange(a.n), np.diff(rp))
+    for perm in (np.arange(len(vals)), np.random.default_rng(3).permutation(len(vals))):
+        b = P.Matrix.from_coo(a.n, a.n, rows[perm], cols[perm], vals[perm])
+        for u, v in zip(a.csr(), b.csr()):
+            assert np.array_equal(u, v)
+    r = [5, 2, 2, 0, 9]
+    c = [1, 3, 3, 0, 0]
+    with pytest.raises(P.FormatError, match=r"^coo: entries not sorted or duplicate at \(2, 3\)$"):
+        P.Matrix.from_coo(6, 6, r, c, [1.0] * 5)  # (9, 0) is out of bounds but sorts last
+    with pytest.raises(P.FormatError, match=r"^coo: entry \(-1, 4\) out of bounds$"):
+        P.Matrix.from_coo(6, 6, r + [-1], c + [4], [1.0] * 6)  # (-1, 4) sorts first
+    with pytest.raises(P.FormatError, match=r"^coo: entry \(1, 6\) out of bounds$"):
+        P.Matrix.from_coo(6, 6, [0, 1, 1], [0, 2, 6], [1.0] * 3)
+    e = P.Matrix.from_coo(3, 3, [], [], [])
+    assert e.shape() == (3, 3, 0)
