@@ -655,7 +655,9 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
     }
     // node-blocked: one lane per neighbour block; else one per entry
     const double work = an->bsr ? off_per_block / (bs * bs) : off_per_block;
-    int lanes = 2;
+    // (4 = the narrowest lane group the sweeps instantiate: the schedule's
+    // items must hold exactly 32 / lanes blocks of the kernel that runs them)
+    int lanes = 4;
     while (lanes < 32 && lanes < work) lanes *= 2;
     if (getenv("PCLAB_LANES")) lanes = atoi(getenv("PCLAB_LANES"));
     // (row-granular level sets are computed on request only: pclab_precond_levels;

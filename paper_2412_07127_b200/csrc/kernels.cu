@@ -310,7 +310,6 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
         if (bc) {
             const int32_t* bcol = bc->bcol.p;
             switch (s.lanes) {
-            case 2:
             case 4: launch_bsr_t<4, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
             case 8: launch_bsr_t<8, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
             case 16: launch_bsr_t<16, BS, UP>(s, bcol, vals, invd, b, x, reset, done, st, pad); break;
@@ -321,7 +320,6 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
     }
     if (rr) {
         switch (s.lanes) {
-            case 2:
             case 4: launch_rr_t<4, BS, UP, 2>(s, M, vals, invd, b, x, reset, done, st); break;
             case 8: launch_rr_t<8, BS, UP, 1>(s, M, vals, invd, b, x, reset, done, st); break;
             case 16: launch_rr_t<16, BS, UP, 2>(s, M, vals, invd, b, x, reset, done, st); break;
@@ -330,7 +328,6 @@ static void launch_trsv_bs(const Schedule& s, const DevCsr& M, bool rr, const Bl
         return;
     }
     switch (s.lanes) {
-        case 2:
         case 4: launch_trsv_t<4, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
         case 8: launch_trsv_t<8, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
         case 16: launch_trsv_t<16, BS, UP>(s, M, vals, invd, b, x, reset, done, ctr, st); break;
@@ -346,6 +343,8 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, boo
     const DevCsr& M = upper ? an.upper : an.lower;
     const BlockCols* bcol = an.bsr ? &(upper ? an.ubc : an.lbc) : nullptr;  // node-blocked sweep
     if (s.nitems == 0) return;
+    if (s.lanes != 4 && s.lanes != 8 && s.lanes != 16 && s.lanes != 32)
+        throw CudaError("sweep schedule built for " + std::to_string(s.lanes) + " lanes per block");
     if (upper) {
         if (an.bs == 3) launch_trsv_bs<3, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);
         else if (an.bs == 2) launch_trsv_bs<2, true>(s, M, an.rr, bcol, vals, invd, b, x, reset, done, ctr, st, pad);

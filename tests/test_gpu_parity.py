@@ -276,6 +276,21 @@ def test_edge_cases():
     assert rep["iterations"] == 1 and abs(x[0] - 1.0) < 1e-15
 
 
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_tiny_2d_poisson_sweeps_and_pcg(m):
+    """Systems whose dof blocks have <= 2 off-block entries (2-D 5-point
+    stencils up to 4 x 4): the sweep schedule is cut for the narrowest lane
+    group the kernels instantiate (round 1 built these for 2 lanes and ran
+    them with 4: the PCG never finished)."""
+    a = P.Matrix.gen_poisson(2, m)
+    oa = O.gen_poisson(2, m)
+    b = P.field_uniform_pm1(a.n, 11)
+    x, rep = P.pcg_solve(a, b, "ic0", rel_tol=1e-10)
+    xo, ro = O.pcg(oa, b, "ic0", rel_tol=1e-10)
+    assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
 def test_error_paths():
     b2 = np.ones(2)
     asym = P.Matrix.from_coo(2, 2, [0, 0, 1, 1], [0, 1, 0, 1], [2.0, 1.0, 0.5, 2.0])
