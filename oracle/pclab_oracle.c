@@ -768,9 +768,21 @@ int or_gnn_forward(int64_t n, const int64_t* rp, const int32_t* cols,
 /* ------------------------------------------------------------------ */
 
 static double dot(int64_t n, const double* a, const double* b) {
+#ifdef OR_DOT_STRIDED
+    /* sensitivity builds only (tests/golden/sensitivity.py): the products
+     * summed in OR_DOT_STRIDED interleaved partial sums, then the partials
+     * in order -- a parallel reduction's association, same terms */
+    double part[OR_DOT_STRIDED];
+    for (int t = 0; t < OR_DOT_STRIDED; ++t) part[t] = 0.0;
+    for (int64_t i = 0; i < n; ++i) part[i % OR_DOT_STRIDED] += a[i] * b[i];
+    double s = 0.0;
+    for (int t = 0; t < OR_DOT_STRIDED; ++t) s += part[t];
+    return s;
+#else
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
+#endif
 }
 
 int or_pcg(int64_t n, const int64_t* rp, const int32_t* cols, const double* vals,

@@ -2,12 +2,15 @@
 
 The C oracle restates the reference's pcg / tri_solve / csr_matvec / ic0
 bit-for-bit (tests/test_oracle.py pins it). This script rebuilds the same
-source with floating-point contraction (gcc -ffp-contract=fast
--march=native: a*b+c fused into one rounding in the dots, the axpys, the
-products and the substitutions -- the arithmetic the device uses) and runs
-the full BASELINE solves with both builds. Same algorithm, same order,
-only the rounding of each multiply-add differs; the iteration counts show
-how far apart two correct implementations land at these sizes.
+source two more ways and runs the full BASELINE solves with each build:
+  * fma_contracted: gcc -ffp-contract=fast -march=native -- a*b+c fused
+    into one rounding in the dots, axpys, products and substitutions (the
+    arithmetic the device uses); same algorithm, same order;
+  * dot_strided_1024: the three dot products per iteration summed in 1024
+    interleaved partials, then the partials in order (a parallel
+    reduction's association; every other operation as the reference).
+The iteration counts show how far apart correct implementations of the
+same algorithm land at these sizes.
 
 Usage (build container, ~15-25 minutes per config on one core):
     python tests/golden/sensitivity.py cfg2     # ic0, configs[2]
@@ -48,14 +51,22 @@ print(json.dumps({{"iterations": int(rep["iterations"]), "converged": int(rep["c
 
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    fma = "/tmp/liboracle_fma.so"
-    subprocess.run(["gcc", "-O2", "-ffp-contract=fast", "-march=native", "-fPIC", "-shared", "-o", fma,
-                    os.path.join(ROOT, "oracle", "pclab_oracle.c"), "-lm"], check=True)
+    src = os.path.join(ROOT, "oracle", "pclab_oracle.c")
+    fma = f"/tmp/liboracle_fma_{which}.so"
+    strided = f"/tmp/liboracle_dot1024_{which}.so"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=fast", "-march=native", "-fPIC", "-shared", "-o", fma, src, "-lm"],
+                   check=True)
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-DOR_DOT_STRIDED=1024", "-fPIC", "-shared", "-o", strided,
+                    src, "-lm"], check=True)
+    from concurrent.futures import ThreadPoolExecutor
+    libs = {"reference_rounding": os.path.join(ROOT, "oracle", "liboracle.so"), "fma_contracted": fma,
+            "dot_strided_1024": strided}
+    with ThreadPoolExecutor(max_workers=int(os.environ.get("SENS_JOBS", "2"))) as ex:
+        futs = {k: ex.submit(run, which, lib) for k, lib in libs.items()}
+        runs = {k: f.result() for k, f in futs.items()}
     res = {"config": which, "kind": "ic0" if which == "cfg2" else "gnnic",
            "note": "same oracle source (bit-identical to the reference when built as oracle/Makefile does) "
-                   "built twice: as the reference (no contraction) and with -ffp-contract=fast -march=native",
-           "reference_rounding": run(which, os.path.join(ROOT, "oracle", "liboracle.so")),
-           "fma_contracted": run(which, fma)}
+                   "built three ways; see the module docstring", **runs}
     with open(os.path.join(HERE, f"sensitivity_{which}.json"), "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps({k: v["iterations"] for k, v in res.items() if isinstance(v, dict)}))
