@@ -9,9 +9,7 @@
 // sync-free in topological order.
 #include <cstdlib>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <cooperative_groups.h>
-#include <cub/device/device_scan.cuh>
 
 #include "core.h"
 
@@ -426,13 +424,6 @@ inline unsigned grid_for(int64_t n, int t) { return static_cast<unsigned>((n + t
 
 }  // namespace
 
-void scan_inplace(int64_t* p, int64_t n, cudaStream_t st) {
-    size_t tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, p, p, n, st);
-    DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-    cub::DeviceScan::ExclusiveSum(t.p, tmp, p, p, n, st);
-    CK(cudaStreamSynchronize(st));
-}
 
 
 void compute_levels(const DevCsr& pred, const DevCsr& succ, int bs, bool upper, Schedule& s,
@@ -525,16 +516,9 @@ static void build_schedule(const DevCsr& pred, const DevCsr& succ, int bs, bool 
     s.order.alloc(nb);
     iota32<<<grid_for(nb, 256), 256, 0, st>>>(idx.p, nb);
     CK_LAUNCH();
-    size_t tmp = 0;
-    const int end_bit = 32;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, s.level.p, sorted_lv.p, idx.p, s.order.p,
-                                    static_cast<int>(nb), 0, end_bit, st);
-    {
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceRadixSort::SortPairs(t.p, tmp, s.level.p, sorted_lv.p, idx.p, s.order.p,
-                                        static_cast<int>(nb), 0, end_bit, st);
-        CK(cudaStreamSynchronize(st));
-    }
+    // levels are non-negative: sort them as unsigned keys
+    radix_sort_pairs(reinterpret_cast<const uint32_t*>(s.level.p), reinterpret_cast<uint32_t*>(sorted_lv.p), idx.p,
+                     s.order.p, nb, 32, st);
     s.nlevels = dev_read(sorted_lv.p + nb - 1, st) + 1;
     DevBuf<int64_t> start(s.nlevels), nit(s.nlevels + 1);
     level_starts<<<grid_for(nb, 256), 256, 0, st>>>(nb, sorted_lv.p, start.p);

@@ -13,8 +13,6 @@
 //     int64 pairs so the reported entry is the reference's first one;
 //   * row pointers by binary search over the sorted rows, int32 columns and
 //     the values gathered through the permutation.
-#include <cub/device/device_radix_sort.cuh>
-
 #include "core.h"
 
 namespace pclab_b200 {
@@ -97,13 +95,6 @@ __global__ void coo_gather(int64_t nnz, const int64_t* __restrict__ c, const dou
     vals[k] = v[s];
 }
 
-template <class K, class V>
-void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, int bits, cudaStream_t st) {
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, bits, st);
-    DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-    cub::DeviceRadixSort::SortPairs(t.p, tmp, kin, kout, vin, vout, n, 0, bits, st);
-}
 
 std::string entry_str(int64_t i, int64_t j) {
     return "(" + std::to_string(i) + ", " + std::to_string(j) + ")";
@@ -143,16 +134,16 @@ std::unique_ptr<Matrix> matrix_from_coo_device(int64_t n_rows, int64_t n_cols, i
             CK_LAUNCH();
             int bits = 1;
             while (bits < 64 && (1ULL << bits) < static_cast<unsigned long long>(n_rows) * n_cols) ++bits;
-            sort_pairs(key.p, skey.p, idx.p, perm.p, nnz, bits, st);
+            radix_sort_pairs(key.p, skey.p, idx.p, perm.p, nnz, bits, st);
         } else {
             // raw signed pairs: stable by column, then stable by row
             iota64<<<gridn(nnz, 256), 256, 0, st>>>(nnz, idx.p);
             coo_signed_key<<<gridn(nnz, 256), 256, 0, st>>>(nnz, c.p, nullptr, key.p);
             CK_LAUNCH();
-            sort_pairs(key.p, skey.p, idx.p, perm.p, nnz, 64, st);
+            radix_sort_pairs(key.p, skey.p, idx.p, perm.p, nnz, 64, st);
             coo_signed_key<<<gridn(nnz, 256), 256, 0, st>>>(nnz, r.p, perm.p, key.p);
             CK_LAUNCH();
-            sort_pairs(key.p, skey.p, perm.p, idx.p, nnz, 64, st);
+            radix_sort_pairs(key.p, skey.p, perm.p, idx.p, nnz, 64, st);
             std::swap(perm, idx);
         }
         DevBuf<unsigned long long> first(1);

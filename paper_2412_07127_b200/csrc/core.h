@@ -193,8 +193,11 @@ T dev_read(const T* d, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     return v;
 }
-// exclusive prefix sum in place (analysis.cu)
+// devsort.cu: exclusive prefix sum in place; stable LSD radix sort of
+// (key, value) pairs on the low `bits` bits of unsigned keys
 void scan_inplace(int64_t* p, int64_t n, cudaStream_t st);
+template <class K, class V>
+void radix_sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, int bits, cudaStream_t st);
 
 // matrices (gen.cu / capi.cpp)
 std::unique_ptr<Matrix> matrix_from_csr_host(int64_t n, const int64_t* rp, const int32_t* cols,

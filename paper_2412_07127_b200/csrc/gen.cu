@@ -7,7 +7,6 @@
 // the values are bit-identical to the reference's. The Q1 elasticity
 // assembly has no reference counterpart; its order is specified by
 // oracle/pclab_oracle.c (or_gen_elasticity) and matched bit for bit.
-#include <cub/device/device_scan.cuh>
 
 #include "core.h"
 
@@ -167,13 +166,6 @@ __global__ void symmetry_check(int64_t n, const int64_t* __restrict__ rp,
     }
 }
 
-void exclusive_scan_inplace(int64_t* counts, int64_t n_plus_1, cudaStream_t st) {
-    size_t tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, counts, n_plus_1, st);
-    DevBuf<unsigned char> t(static_cast<int64_t>(tmp));
-    cub::DeviceScan::ExclusiveSum(t.p, tmp, counts, counts, n_plus_1, st);
-    CK(cudaStreamSynchronize(st));
-}
 
 int64_t read_i64(const int64_t* d, cudaStream_t st) {
     int64_t v;
@@ -241,7 +233,7 @@ std::unique_ptr<Matrix> gen_poisson_device(int dim, int64_t m, const double* cel
     poisson_rows<false><<<g, T, 0, st>>>(dim, m, k.p, a.rp.p, nullptr, nullptr, n);
     CK_LAUNCH();
     CK(cudaMemsetAsync(a.rp.p + n, 0, sizeof(int64_t), st));
-    exclusive_scan_inplace(a.rp.p, n + 1, st);
+    scan_inplace(a.rp.p, n + 1, st);
     a.nnz = read_i64(a.rp.p + n, st);
     a.cols.alloc(a.nnz);
     a.vals.alloc(a.nnz);
@@ -272,7 +264,7 @@ std::unique_ptr<Matrix> gen_elasticity_device(int64_t m, double nu, const double
     elasticity_rows<false><<<g, T, 0, st>>>(m, mod.p, a.rp.p, nullptr, nullptr, n);
     CK_LAUNCH();
     CK(cudaMemsetAsync(a.rp.p + n, 0, sizeof(int64_t), st));
-    exclusive_scan_inplace(a.rp.p, n + 1, st);
+    scan_inplace(a.rp.p, n + 1, st);
     a.nnz = read_i64(a.rp.p + n, st);
     a.cols.alloc(a.nnz);
     a.vals.alloc(a.nnz);

@@ -37,8 +37,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include "core.h"
 #include "sweep.cuh"
 
@@ -615,12 +613,9 @@ void build_one(const Analysis& an, const Schedule& s, RangeSched& rs, cudaStream
     rs_keys<<<gridn(nb, 256), 256, 0, st>>>(nb, UPPER, R, s.level.p, key.p, val.p);
     CK_LAUNCH();
     {
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, skey.p, val.p, rs.order.p, static_cast<int>(nb), 0, 64,
-                                        st);
-        DevBuf<unsigned char> t(static_cast<int64_t>(tmp) + 1);
-        cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, skey.p, val.p, rs.order.p, static_cast<int>(nb), 0, 64, st);
-        CK(cudaStreamSynchronize(st));
+        int bits = 32;
+        while (bits < 64 && (1LL << (bits - 32)) < rs.nranges) ++bits;
+        radix_sort_pairs(key.p, skey.p, val.p, rs.order.p, nb, bits, st);
     }
     // groups
     DevBuf<int64_t> gid(nb + 1);

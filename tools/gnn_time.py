@@ -1,5 +1,6 @@
-"""Developer probe: wall time of the IC(0) and gnnic preconditioner builds
-(the difference is the GNN forward pass) on one workload."""
+"""Developer probe: device time of the IC(0) and gnnic preconditioner
+builds on one workload, with and without a fresh symbolic analysis, and
+the per-phase split the library reports (Precond.timings())."""
 import os
 import sys
 import time
@@ -12,11 +13,13 @@ import paper_2412_07127_b200 as P  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "elasticity_q1_118"
 w = P.workloads.by_name(name)
 a, b, model = P.workloads.build(w)
-P.Precond(a, "ic0")
-P.Precond(a, "gnnic", model)
-for kind in ("ic0", "gnnic", "ic0", "gnnic"):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    P.Precond(a, kind, model if kind == "gnnic" else None)
-    torch.cuda.synchronize()
-    print(kind, f"{(time.perf_counter() - t0) * 1e3:.1f} ms", flush=True)
+for drop in (False, True, False, True, True):
+    for kind in ("ic0", "gnnic"):
+        if drop:
+            a.drop_analysis()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pc = P.Precond(a, kind, model if kind == "gnnic" else None)
+        torch.cuda.synchronize()
+        print(kind, "drop" if drop else "keep", f"{(time.perf_counter() - t0) * 1e3:.1f} ms", pc.timings(), flush=True)
+        del pc
