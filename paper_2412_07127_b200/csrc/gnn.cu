@@ -68,21 +68,24 @@ __global__ void degree_kernel(int64_t n, const int64_t* __restrict__ rp,
     if (i < n) deg[i] = static_cast<double>(rp[i + 1] - rp[i] - (dpos[i] >= 0 ? 1 : 0));
 }
 
-// Warp per row (lanes over the entries, coalesced): diagonal, |off| sum and
-// max, neighbour-degree max / min / mean, then their variance from the
-// row's entries again (L1-resident). Sums are fixed shuffle trees (the
-// reference adds in entry order; the features differ from it by rounding
-// only, and the degrees and their mean are exact integers / quotients).
+// FL lanes per row (lanes over the entries, coalesced; 32 / FL rows per
+// warp): diagonal, |off| sum and max, neighbour-degree max / min / mean,
+// then their variance from the row's entries again (L1-resident). Sums are
+// fixed shuffle trees (the reference adds in entry order; the features
+// differ from it by rounding only, and the degrees and their mean are
+// exact integers / quotients). Measured on configs[2] (81 entries per row):
+// 32 lanes per row 4.4 ms (issue-bound on the per-row reductions and tail).
+constexpr int FL = 8;
 __global__ void __launch_bounds__(256)
 features_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
                 const double* __restrict__ vals, const double* __restrict__ deg, double* __restrict__ f) {
-    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int64_t b = rp[i], e = rp[i + 1];
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / FL;
+    const int gl = threadIdx.x % FL;
+    const bool act = i < n;
+    const int64_t b = act ? rp[i] : 0, e = act ? rp[i + 1] : 0;
     double diag = 0.0, osum = 0.0, omax = 0.0, mx = 0.0, mn = 1e300, dsum = 0.0;
     int cnt = 0;
-    for (int64_t k = b + lane; k < e; k += 32) {
+    for (int64_t k = b + gl; k < e; k += FL) {
         const double av = fabs(vals[k]);
         const int32_t j = cols[k];
         if (j == i) {
@@ -98,32 +101,31 @@ features_kernel(int64_t n, const int64_t* __restrict__ rp, const int32_t* __rest
         ++cnt;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        diag += __shfl_xor_sync(0xffffffffu, diag, o);  // one lane holds it
-        osum += __shfl_xor_sync(0xffffffffu, osum, o);
-        omax = fmax(omax, __shfl_xor_sync(0xffffffffu, omax, o));
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    for (int o = FL / 2; o > 0; o >>= 1) {
+        diag += __shfl_xor_sync(0xffffffffu, diag, o, FL);  // one lane holds it
+        osum += __shfl_xor_sync(0xffffffffu, osum, o, FL);
+        omax = fmax(omax, __shfl_xor_sync(0xffffffffu, omax, o, FL));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o, FL));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o, FL));
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o, FL);
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o, FL);
     }
-    double var = 0.0, mean = 0.0;
-    if (cnt > 0) {
-        mean = dsum / static_cast<double>(cnt);
-        for (int64_t k = b + lane; k < e; k += 32) {
+    const double mean = cnt > 0 ? dsum / static_cast<double>(cnt) : 0.0;
+    double var = 0.0;
+    if (cnt > 0)
+        for (int64_t k = b + gl; k < e; k += FL) {
             const int32_t j = cols[k];
             if (j == i) continue;
             const double dd = deg[j] - mean;
             var += dd * dd;
         }
-        var = group_sum<32>(var);
-    }
-    if (lane == 0) {
+    var = group_sum<FL>(var);
+    if (act && gl == 0) {
         double* row = f + i * kF;
         row[0] = deg[i];
         row[1] = cnt > 0 ? mx : 0.0;
         row[2] = cnt > 0 ? mn : 0.0;
-        row[3] = cnt > 0 ? mean : 0.0;
+        row[3] = mean;
         row[4] = cnt > 0 ? var / static_cast<double>(cnt) : 0.0;
         const double denom = diag + osum;
         row[5] = denom > 0.0 ? diag / denom : 0.0;
@@ -373,7 +375,7 @@ void gnn_forward(const Matrix& A, const Analysis& an, const Model& model, double
     // ---- node features (features.cpp:11-72)
     DevBuf<double> deg(n), feat(n * kF), x0(n * kF), cnt(n);
     degree_kernel<<<gfor(n, T), T, 0, st>>>(n, A.a.rp.p, A.diag_pos.p, deg.p);
-    features_kernel<<<gfor(n * 32, T), T, 0, st>>>(n, A.a.rp.p, A.a.cols.p, A.a.vals.p, deg.p, feat.p);
+    features_kernel<<<gfor(n * FL, T), T, 0, st>>>(n, A.a.rp.p, A.a.cols.p, A.a.vals.p, deg.p, feat.p);
     CK_LAUNCH();
     // ---- graph normalisation statistics (gnn.cpp:141-160)
     const int parts = sm_count() * 2;
