@@ -699,8 +699,10 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
             }
         }
     }
-    // range-pipelined sweeps (range.cu) on the final sweep layout
+    // range-pipelined sweeps (range.cu) and the item-ordered value streams
+    // (bss.cu) on the final sweep layout
     build_range_scheds(*an, st);
+    build_bss(*an, st);
     // node-blocked A: the PCG product reads one column index per block
     an->a_bsr = false;
     if (an->bsr) {

@@ -1,0 +1,153 @@
+// Item-ordered value streams of the node-blocked sweeps (bss_trsv_kernel,
+// sweep.cuh): per slot of a sweep schedule (Schedule::slots, 2 blocks per
+// warp item), a 16-byte header and the block's neighbour ids (per
+// analysis), and the block's factor values re-laid block-major (per
+// factor: a gather from the L / U values after every factor build).
+#include "core.h"
+#include "sweep.cuh"
+
+namespace pclab_b200 {
+
+namespace {
+
+inline unsigned gridn(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+__global__ void bss_lengths(int64_t ns, const int32_t* __restrict__ slots, const int64_t* __restrict__ bp,
+                            int64_t* __restrict__ lv, int64_t* __restrict__ lc) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s > ns) return;
+    if (s == ns) {
+        lv[s] = lc[s] = 0;
+        return;
+    }
+    const int32_t b = slots[s];
+    const int64_t nb = b >= 0 ? bp[b + 1] - bp[b] : 0;
+    lv[s] = b >= 0 ? 9 * nb + 6 : 0;
+    lc[s] = nb;
+}
+
+// headers and neighbour block ids (warp per slot)
+__global__ void bss_headers(int64_t ns, const int32_t* __restrict__ slots, const int64_t* __restrict__ bp,
+                            const int32_t* __restrict__ bcol, const int64_t* __restrict__ voff,
+                            const int64_t* __restrict__ coff, int4* __restrict__ hdr, int32_t* __restrict__ scol) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int32_t b = slots[s];
+    const int64_t nb = b >= 0 ? bp[b + 1] - bp[b] : 0;
+    if (lane == 0)
+        hdr[s] = make_int4(b, static_cast<int>(nb), static_cast<int>(static_cast<uint32_t>(voff[s])),
+                           static_cast<int>(static_cast<uint32_t>(coff[s])));
+    for (int64_t n = lane; n < nb; n += 32) scol[coff[s] + n] = bcol[bp[b] + n] / 3;
+}
+
+// values of one slot (warp per slot): neighbour n's 3x3 block at 9n (row
+// t, column c at 3t + c), then the in-block entries in solve_diag_block's
+// order, then 1 / l_tt
+template <bool UPPER>
+__global__ void bss_values(int64_t ns, const int4* __restrict__ hdr, const int64_t* __restrict__ rp,
+                           const double* __restrict__ vals, const double* __restrict__ invd,
+                           double* __restrict__ sval) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int4 h = hdr[s];
+    if (h.x < 0) return;
+    const int64_t b = h.x;
+    const int nb = h.y;
+    double* v = sval + static_cast<uint32_t>(h.z);
+    for (int idx = lane; idx < 9 * nb; idx += 32) {
+        const int n = idx / 9, w = idx % 9, t = w / 3, c = w % 3;
+        v[idx] = vals[rp[3 * b + t] + (UPPER ? 3 - t : 0) + 3 * n + c];
+    }
+    if (lane == 0) {
+        double* d = v + 9 * nb;
+        int q = 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (!UPPER && c < t) d[q++] = vals[rp[3 * b + t + 1] - (t + 1) + c];
+                if (UPPER && c > t) d[q++] = vals[rp[3 * b + t] + (c - t)];
+            }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) d[3 + t] = invd[3 * b + t];
+    }
+}
+
+void build_one(Schedule& s, const BlockCols& bc, cudaStream_t st) {
+    s.bss = false;
+    if (s.lanes != 16 || s.per_item != 2) return;
+    const int64_t ns = s.nitems * s.per_item;
+    if (ns == 0 || ns >= (1LL << 31)) return;
+    DevBuf<int64_t> voff(ns + 1), coff(ns + 1);
+    bss_lengths<<<gridn(ns + 1, 256), 256, 0, st>>>(ns, s.slots.p, bc.bp.p, voff.p, coff.p);
+    CK_LAUNCH();
+    scan_inplace(voff.p, ns + 1, st);
+    scan_inplace(coff.p, ns + 1, st);
+    const int64_t nv = dev_read(voff.p + ns, st), nc = dev_read(coff.p + ns, st);
+    if (nv >= (1LL << 32) || nc >= (1LL << 32)) return;
+    s.bss_hdr.alloc(ns);
+    s.bss_col.alloc(std::max<int64_t>(nc, 1));
+    bss_headers<<<gridn(ns * 32, 256), 256, 0, st>>>(ns, s.slots.p, bc.bp.p, bc.bcol.p, voff.p, coff.p,
+                                                    s.bss_hdr.p, s.bss_col.p);
+    CK_LAUNCH();
+    s.bss_nvals = nv;
+    s.bss = true;
+}
+
+}  // namespace
+
+bool bss_enabled() {
+    static const bool on = !(getenv("PCLAB_BSS") && atoi(getenv("PCLAB_BSS")) == 0);
+    return on;
+}
+
+void build_bss(Analysis& an, cudaStream_t st) {
+    an.blk_lo.bss = an.blk_up.bss = false;
+    if (!bss_enabled() || !an.bsr || an.bs != 3) return;
+    build_one(an.blk_lo, an.lbc, st);
+    build_one(an.blk_up, an.ubc, st);
+    if (!(an.blk_lo.bss && an.blk_up.bss)) an.blk_lo.bss = an.blk_up.bss = false;
+}
+
+void fill_bss(const Analysis& an, Precond& p, cudaStream_t st) {
+    if (!an.blk_lo.bss) return;
+    for (int up = 0; up < 2; ++up) {
+        const Schedule& s = up ? an.blk_up : an.blk_lo;
+        DevBuf<double>& out = up ? p.bss_up : p.bss_lo;
+        out.alloc(std::max<int64_t>(s.bss_nvals, 1));
+        const int64_t ns = s.nitems * s.per_item;
+        if (up)
+            bss_values<true><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, s.bss_hdr.p, an.upper.rp.p, p.uvals.p,
+                                                                 p.invd.p, out.p);
+        else
+            bss_values<false><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, s.bss_hdr.p, an.lower.rp.p, p.lvals.p,
+                                                                  p.invd.p, out.p);
+        CK_LAUNCH();
+    }
+}
+
+bool launch_bss(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
+                const int* done, cudaStream_t st, bool pad) {
+    const Schedule& s = upper ? an.blk_up : an.blk_lo;
+    const double* sv = upper ? p.bss_up.p : p.bss_lo.p;
+    if (!pad || !s.bss || !sv || s.nitems == 0) return false;
+    auto kern = upper ? bss_trsv_kernel<true> : bss_trsv_kernel<false>;
+    static unsigned cap[2] = {0, 0};
+    if (!cap[upper]) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BSR_THREADS, 0));
+        cap[upper] = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+    }
+    // every warp resident (round-robin items), ~5 levels of items in flight
+    const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
+    const int64_t warps = static_cast<int64_t>(5.0 * per_level) + 1;
+    const int64_t blocks = std::max<int64_t>((warps + BSR_THREADS / 32 - 1) / (BSR_THREADS / 32), sm_count());
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, cap[upper]));
+    kern<<<grid, BSR_THREADS, 0, st>>>(static_cast<int>(s.nitems), s.bss_hdr.p, s.bss_col.p, sv, b, x, reset, done);
+    CK_LAUNCH();
+    return true;
+}
+
+}  // namespace pclab_b200

@@ -84,6 +84,11 @@ struct Schedule {
     DevBuf<int32_t> slot_rp;     // [nitems * per_item * 4] 16-byte slot records {block (-1 idle),
                                  //  first row pointer, first block column, row lengths 10 bits each}
     int64_t max_level_width = 0;
+    // item-ordered value stream of the node-blocked sweep (bss.cu)
+    bool bss = false;
+    int64_t bss_nvals = 0;
+    DevBuf<int4> bss_hdr;     // [slots] {block, neighbours, value offset, column offset}
+    DevBuf<int32_t> bss_col;  // neighbour block ids, slot after slot
 };
 
 // Block-column view of a node-blocked CSR matrix (Analysis::bsr): block
@@ -165,6 +170,7 @@ struct Precond {
     DevBuf<double> uvals;       // same values on U's pattern (gathered)
     DevBuf<double> invd;        // 1 / l_ii (both sweeps)
     DevBuf<unsigned char> stream_lo, stream_up;  // range-sweep streams (RangeSched)
+    DevBuf<double> bss_lo, bss_up;               // item-ordered sweep values (bss.cu)
     DevBuf<double> diag;        // Jacobi payload
     double sigma = 1.0;         // GNN edge scale
     int ic0_attempts = 0;
@@ -237,6 +243,11 @@ struct Precond;
 void trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, cudaStream_t st);
 void launch_trsv(const Analysis& an, const double* vals, const double* invd, bool upper, const double* b,
                  double* x, double* reset, const int* done, unsigned* ctr, cudaStream_t st, bool pad = false);
+// bss.cu: item-ordered value streams of the node-blocked sweeps
+void build_bss(Analysis& an, cudaStream_t st);
+void fill_bss(const Analysis& an, Precond& p, cudaStream_t st);
+bool launch_bss(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
+                const int* done, cudaStream_t st, bool pad);
 // range.cu: range-pipelined sweeps
 void build_range_scheds(Analysis& an, cudaStream_t st);
 void fill_range_streams(const Analysis& an, Precond& p, cudaStream_t st);

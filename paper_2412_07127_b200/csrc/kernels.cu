@@ -363,6 +363,7 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, boo
 void launch_sweep(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
                   const int* done, unsigned* ctr, cudaStream_t st, bool pad) {
     if (launch_range_trsv(an, p, upper, b, x, reset, done, st, pad)) return;
+    if (launch_bss(an, p, upper, b, x, reset, done, st, pad)) return;
     launch_trsv(an, upper ? p.uvals.p : p.lvals.p, p.invd.p, upper, b, x, reset, done, ctr, st, pad);
 }
 

@@ -675,6 +675,118 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
                                   (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
 }
 
+// ------------------------------------------------------------------------
+// Node-blocked sweep on the item-ordered stream (bss.cu): the 3x3 node-
+// blocked, padded PCG-loop case of bsr_trsv_kernel with the factor values
+// re-laid per slot of the schedule -- a slot's block holds its neighbour
+// blocks' 9 values contiguously (block-major, row-major inside a block),
+// then the 3 strictly-lower / -upper in-block entries and the 3 reciprocal
+// pivots -- and the neighbour block ids beside them. A slot is one 16-byte
+// header {block, neighbours, value offset, column offset}; every address of
+// an item is that header plus an immediate, and one L1 prefetch per lane
+// covers the next item's values. Same lane mapping, FMA order, shuffle tree
+// and diagonal solve as bsr_item: bit-identical results.
+#ifndef BSS_CTAS
+#define BSS_CTAS 7
+#endif
+template <bool UPPER>
+__global__ void __launch_bounds__(BSR_THREADS, BSS_CTAS)
+bss_trsv_kernel(int nitems, const int4* __restrict__ hdr, const int32_t* __restrict__ scol,
+                const double* __restrict__ sval, const double* rhs, double* out, double* reset,
+                const int* __restrict__ done) {
+    if (done && *done) return;
+    constexpr int BS = 3, LG = 16, G = 2, NIB = 3;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    int it = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    auto hdr_at = [&](int i) { return i < nitems ? __ldg(hdr + (i * G + grp)) : make_int4(-1, 0, 0, 0); };
+    int4 h = hdr_at(it), h1 = hdr_at(it + nw), h2 = hdr_at(it + 2 * nw);
+    // a block's values span <= 9 * 16 + 6 doubles: one 128-byte line per
+    // lane (lines from the one holding the first value)
+    auto prefetch = [&](const int4& q) {
+        if (q.x >= 0) {
+            const uintptr_t v0 = reinterpret_cast<uintptr_t>(sval + static_cast<uint32_t>(q.z));
+            const uintptr_t v1 = v0 + 8 * static_cast<uintptr_t>(9 * q.y + 6);
+            const uintptr_t a = (v0 & ~uintptr_t(127)) + 128 * static_cast<uintptr_t>(gl);
+            if (a < v1) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(scol + static_cast<uint32_t>(q.w)));
+        }
+    };
+    prefetch(h);
+    while (it < nitems) {
+        prefetch(h1);
+        const bool active = h.x >= 0;
+        const int64_t blk = active ? h.x : 0;
+        const int nb = active ? h.y : 0;
+        const double* v = sval + static_cast<uint32_t>(h.z);
+        const int32_t* c = scol + static_cast<uint32_t>(h.w);
+        double rc[BS] = {0.0, 0.0, 0.0}, bin[NIB], binv[BS];
+        if (active && gl == 0) {
+            if constexpr (UPPER) {  // padded y: one 256-bit load
+                double d3;
+                asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                             : "=d"(rc[0]), "=d"(rc[1]), "=d"(rc[2]), "=d"(d3)
+                             : "l"(rhs + 4 * blk));
+                (void)d3;
+            } else {
+#pragma unroll
+                for (int t = 0; t < BS; ++t) rc[t] = rhs[blk * BS + t];
+            }
+#pragma unroll
+            for (int j = 0; j < NIB; ++j) bin[j] = __ldg(v + 9 * nb + j);
+#pragma unroll
+            for (int t = 0; t < BS; ++t) binv[t] = __ldg(v + 9 * nb + NIB + t);
+        }
+        double acc[BS] = {0.0, 0.0, 0.0};
+        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
+        for (int n0 = 0; n0 < nbmax; n0 += LG) {
+            const int n = n0 + gl;
+            const bool own = n < nb;
+            double a[BS][BS], xv[BS] = {0.0, 0.0, 0.0};
+            int32_t xb = 0;
+            if (own) {
+                xb = __ldg(c + n);
+                const double* vn = v + 9 * n;
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) a[t][cc] = __ldg(vn + BS * t + cc);
+                ld_relaxed_v4(out + 4 * static_cast<int64_t>(xb), xv);
+            } else {
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+#pragma unroll
+                    for (int cc = 0; cc < BS; ++cc) a[t][cc] = 0.0;
+            }
+            bool pend = own && (is_pending(xv[0]) || is_pending(xv[1]) || is_pending(xv[2]));
+            while (__any_sync(0xffffffffu, pend)) {
+                if (pend) {
+                    ld_relaxed_v4(out + 4 * static_cast<int64_t>(xb), xv);
+                    pend = is_pending(xv[0]) || is_pending(xv[1]) || is_pending(xv[2]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < BS; ++t)
+#pragma unroll
+                for (int cc = 0; cc < BS; ++cc) acc[t] = fma(a[t][cc], xv[cc], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+        if (active && gl == 0) {
+            double x[BS];
+            solve_diag_block<BS, UPPER>(rc, acc, bin, binv, x);
+            st_relaxed_v4(out + 4 * blk, x[0], x[1], x[2], 0.0);
+        }
+        __syncwarp();
+        if (reset && active && gl < BS) reset[4 * blk + gl] = pending_value();
+        it += nw;
+        h = h1;
+        h1 = h2;
+        h2 = hdr_at(it + 2 * nw);
+    }
+}
+
 // Round-robin sweep for matrices that are not node-blocked (Poisson, FV
 // diffusion): the scheduling of bsr_sweep -- items dealt round-robin to all
 // resident warps, slot records two items ahead, entries prefetched into L1

@@ -19,6 +19,11 @@ device at full size:
     reference's gnn_forward / gnn_ic_predict / pcg on the committed small
     fixtures (tests/test_oracle.py). Keys record which one produced what
     (`<tag>.source`).
+* configs[3] (Q1 elasticity 149^3, 10,062,150 dofs, lognormal(0, 1.5)):
+  IC(0) breaks down after the reference's three shifts, so ic0 and gnnic
+  fail; the NIC factor (nic_predict, precond.cpp:145) at 4096 seeded
+  entries and what PCG does with it, from the C oracle (the reference's
+  gnn_forward does not fit the build container's memory at this size).
 * configs[4] (7-point FV diffusion 256^3, 16,777,216 dofs): gnnic PCG to
   rtol 1e-8, max 5000 iterations: the same solve record, plus the GNN-
   corrected factor at 4096 seeded entries.
@@ -31,6 +36,7 @@ assembly is the reference's own arithmetic.
 Usage (build container only, needs /root/reference and ~30 GB RAM; each
 config takes 10-25 minutes on one core):
     python tests/golden/make_fullsize.py cfg2
+    python tests/golden/make_fullsize.py cfg3
     python tests/golden/make_fullsize.py cfg4
 Writes tests/golden/fullsize_<cfg>.npz.
 """
@@ -105,7 +111,7 @@ def main():
         raise SystemExit("oracle/_ref not built: make -C oracle")
     from paper_2412_07127_b200 import workloads as W
 
-    cfg = {"cfg2": CONFIGS[2], "cfg4": CONFIGS[4]}[which]
+    cfg = {"cfg2": CONFIGS[2], "cfg3": CONFIGS[3], "cfg4": CONFIGS[4]}[which]
     t0 = time.time()
     a, b, params = W.build_oracle(cfg)
     print(which, "n", a.n, "nnz", a.nnz, f"built in {time.time() - t0:.0f} s", flush=True)
@@ -119,6 +125,10 @@ def main():
         solve_record(d, "pcg.gnnic", a, b, "gnnic", params, -1, use_oracle=True)
         factor_record(d, "ic0", a, "ic0", None, lidx)
         solve_record(d, "pcg.ic0", a, b, "ic0", None, -1)
+    elif which == "cfg3":
+        factor_record(d, "ic0", a, "ic0", None, lidx, use_oracle=True)
+        factor_record(d, "nic", a, "nic", params, lidx, use_oracle=True)
+        solve_record(d, "pcg.nic", a, b, "nic", params, 20, use_oracle=True)
     else:
         factor_record(d, "gnnic", a, "gnnic", params, lidx)
         solve_record(d, "pcg.gnnic", a, b, "gnnic", params, cfg.max_iters)

@@ -77,3 +77,43 @@ def test_ic0_mask_kernel_bit_identical_to_merge_walk():
         assert out.returncode == 0, out.stdout + out.stderr
         outs.append(out.stdout.strip())
     assert len(set(outs)) == 1, outs
+
+
+SWEEP_BITS = r"""
+import hashlib, sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+import paper_2412_07127_b200 as P
+h = hashlib.sha256()
+w = P.workloads.by_name("elasticity_q1_40").scaled(12)
+a, b, model = P.workloads.build(w)
+for kind in ("ic0", "gnnic"):
+    pc = P.Precond(a, kind, model if kind == "gnnic" else None)
+    r = torch.from_numpy(np.random.default_rng(2).standard_normal(a.n)).cuda()
+    y = torch.empty_like(r)
+    for upper in (False, True):
+        pc.trsv_device(upper, r.data_ptr(), y.data_ptr())
+        h.update(y.cpu().numpy().tobytes())
+    bt = torch.from_numpy(b).cuda()
+    xt = torch.zeros_like(bt)
+    rep = pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=1e-8, max_iters=300)
+    h.update(xt.cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_item_stream_sweep_bit_identical_to_csr_sweep():
+    """bss_trsv_kernel (factor values re-laid per schedule slot, bss.cu) and
+    bsr_trsv_kernel (values read from the L / U CSR, PCLAB_BSS=0) use the
+    same lane mapping, FMA order, shuffle tree and diagonal solve: both
+    sweeps and whole PCG solves are bit-identical."""
+    outs = []
+    for env in ({"PCLAB_BSS": "0"}, {}):
+        e = dict(os.environ, **env)
+        out = subprocess.run([sys.executable, "-c", SWEEP_BITS.format(root=ROOT)], env=e, cwd=ROOT,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stdout + out.stderr
+        outs.append(out.stdout.strip())
+    assert len(set(outs)) == 1, outs
+
