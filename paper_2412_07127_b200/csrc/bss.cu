@@ -75,6 +75,110 @@ __global__ void bss_values(int64_t ns, const int4* __restrict__ hdr, const int64
     }
 }
 
+// ---- scalar (entry-lane) slots: block rows r0 .. r0+bs-1 of L (diagonal
+// last) or U (diagonal first); a slot's off-block entries in row order
+__device__ __forceinline__ void slot_rows_of(const int64_t* rp, int64_t b, int bs, bool upper, int64_t* ob, int* oc) {
+    for (int t = 0; t < bs; ++t) {
+        const int64_t r = b * bs + t;
+        ob[t] = upper ? rp[r] + (bs - t) : rp[r];
+        oc[t] = static_cast<int>(upper ? rp[r + 1] - ob[t] : rp[r + 1] - (t + 1) - rp[r]);
+    }
+}
+
+__global__ void rrs_lengths(int64_t ns, int bs, bool upper, const int32_t* __restrict__ slots,
+                            const int64_t* __restrict__ rp, int64_t* __restrict__ lv, int64_t* __restrict__ lc) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (s > ns) return;
+    if (s == ns) {
+        lv[s] = lc[s] = 0;
+        return;
+    }
+    const int32_t b = slots[s];
+    int64_t ob[3];
+    int oc[3], tot = 0;
+    if (b >= 0) {
+        slot_rows_of(rp, b, bs, upper, ob, oc);
+        for (int t = 0; t < bs; ++t) tot += oc[t];
+    }
+    lv[s] = b >= 0 ? tot + bs * (bs - 1) / 2 + bs : 0;
+    lc[s] = tot;
+}
+
+__global__ void rrs_headers(int64_t ns, int bs, bool upper, const int32_t* __restrict__ slots,
+                            const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                            const int64_t* __restrict__ voff, const int64_t* __restrict__ coff,
+                            int4* __restrict__ hdr, int32_t* __restrict__ code) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int32_t b = slots[s];
+    int64_t ob[3];
+    int oc[3], tot = 0;
+    if (b >= 0) {
+        slot_rows_of(rp, b, bs, upper, ob, oc);
+        for (int t = 0; t < bs; ++t) tot += oc[t];
+    }
+    if (lane == 0)
+        hdr[s] = make_int4(b, tot, static_cast<int>(static_cast<uint32_t>(voff[s])),
+                           static_cast<int>(static_cast<uint32_t>(coff[s])));
+    int base = 0;
+    for (int t = 0; t < bs && b >= 0; ++t) {
+        for (int e = lane; e < oc[t]; e += 32) code[coff[s] + base + e] = (cols[ob[t] + e] << 2) | t;
+        base += oc[t];
+    }
+}
+
+template <bool UPPER>
+__global__ void rrs_values(int64_t ns, int bs, const int4* __restrict__ hdr, const int64_t* __restrict__ rp,
+                           const double* __restrict__ vals, const double* __restrict__ invd,
+                           double* __restrict__ sval) {
+    const int64_t s = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int4 h = hdr[s];
+    if (h.x < 0) return;
+    const int64_t b = h.x;
+    int64_t ob[3];
+    int oc[3];
+    slot_rows_of(rp, b, bs, UPPER, ob, oc);
+    double* v = sval + static_cast<uint32_t>(h.z);
+    int base = 0;
+    for (int t = 0; t < bs; ++t) {
+        for (int e = lane; e < oc[t]; e += 32) v[base + e] = vals[ob[t] + e];
+        base += oc[t];
+    }
+    if (lane == 0) {
+        double* d = v + base;
+        int q = 0;
+        for (int t = 0; t < bs; ++t)
+            for (int c = 0; c < bs; ++c) {
+                if (!UPPER && c < t) d[q++] = vals[rp[b * bs + t + 1] - (t + 1) + c];
+                if (UPPER && c > t) d[q++] = vals[rp[b * bs + t] + (c - t)];
+            }
+        for (int t = 0; t < bs; ++t) d[q + t] = invd[b * bs + t];
+    }
+}
+
+void build_one_scalar(Schedule& s, const DevCsr& M, int bs, bool upper, cudaStream_t st) {
+    s.bss = false;
+    const int64_t ns = s.nitems * s.per_item;
+    if (ns == 0 || ns >= (1LL << 31) || bs > 3) return;
+    DevBuf<int64_t> voff(ns + 1), coff(ns + 1);
+    rrs_lengths<<<gridn(ns + 1, 256), 256, 0, st>>>(ns, bs, upper, s.slots.p, M.rp.p, voff.p, coff.p);
+    CK_LAUNCH();
+    scan_inplace(voff.p, ns + 1, st);
+    scan_inplace(coff.p, ns + 1, st);
+    const int64_t nv = dev_read(voff.p + ns, st), nc = dev_read(coff.p + ns, st);
+    if (nv >= (1LL << 32) || nc >= (1LL << 32) || M.n >= (1LL << 29)) return;
+    s.bss_hdr.alloc(ns);
+    s.bss_col.alloc(std::max<int64_t>(nc, 1));
+    rrs_headers<<<gridn(ns * 32, 256), 256, 0, st>>>(ns, bs, upper, s.slots.p, M.rp.p, M.cols.p, voff.p, coff.p,
+                                                    s.bss_hdr.p, s.bss_col.p);
+    CK_LAUNCH();
+    s.bss_nvals = nv;
+    s.bss = true;
+}
+
 void build_one(Schedule& s, const BlockCols& bc, cudaStream_t st) {
     s.bss = false;
     if (s.lanes != 16 || s.per_item != 2) return;
@@ -105,9 +209,14 @@ bool bss_enabled() {
 
 void build_bss(Analysis& an, cudaStream_t st) {
     an.blk_lo.bss = an.blk_up.bss = false;
-    if (!bss_enabled() || !an.bsr || an.bs != 3) return;
-    build_one(an.blk_lo, an.lbc, st);
-    build_one(an.blk_up, an.ubc, st);
+    if (!bss_enabled()) return;
+    if (an.bsr && an.bs == 3) {
+        build_one(an.blk_lo, an.lbc, st);
+        build_one(an.blk_up, an.ubc, st);
+    } else if (!an.bsr && an.rr) {
+        build_one_scalar(an.blk_lo, an.lower, an.bs, false, st);
+        build_one_scalar(an.blk_up, an.upper, an.bs, true, st);
+    }
     if (!(an.blk_lo.bss && an.blk_up.bss)) an.blk_lo.bss = an.blk_up.bss = false;
 }
 
@@ -118,6 +227,16 @@ void fill_bss(const Analysis& an, Precond& p, cudaStream_t st) {
         DevBuf<double>& out = up ? p.bss_up : p.bss_lo;
         out.alloc(std::max<int64_t>(s.bss_nvals, 1));
         const int64_t ns = s.nitems * s.per_item;
+        if (!an.bsr) {
+            if (up)
+                rrs_values<true><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, an.bs, s.bss_hdr.p, an.upper.rp.p,
+                                                                     p.uvals.p, p.invd.p, out.p);
+            else
+                rrs_values<false><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, an.bs, s.bss_hdr.p, an.lower.rp.p,
+                                                                      p.lvals.p, p.invd.p, out.p);
+            CK_LAUNCH();
+            continue;
+        }
         if (up)
             bss_values<true><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, s.bss_hdr.p, an.upper.rp.p, p.uvals.p,
                                                                  p.invd.p, out.p);
@@ -128,11 +247,54 @@ void fill_bss(const Analysis& an, Precond& p, cudaStream_t st) {
     }
 }
 
+template <int LG, int BS, bool UP, int CH>
+void launch_rrs_t(const Schedule& s, const double* sv, const double* b, double* x, double* reset, const int* done,
+                  cudaStream_t st) {
+    static unsigned cap = 0;
+    if (!cap) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rrs_trsv_kernel<LG, BS, UP, CH>, RR_THREADS, 0));
+        cap = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+    }
+    const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
+    const int64_t warps = static_cast<int64_t>(6.0 * per_level) + 1;
+    const int64_t blocks = std::max<int64_t>((warps + RR_THREADS / 32 - 1) / (RR_THREADS / 32), sm_count());
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, cap));
+    rrs_trsv_kernel<LG, BS, UP, CH><<<grid, RR_THREADS, 0, st>>>(s.nitems, s.bss_hdr.p, s.bss_col.p, sv, b, x,
+                                                                 reset, done);
+    CK_LAUNCH();
+}
+
+template <int BS, bool UP>
+void launch_rrs_bs(const Schedule& s, const double* sv, const double* b, double* x, double* reset, const int* done,
+                   cudaStream_t st) {
+    switch (s.lanes) {
+        case 4: launch_rrs_t<4, BS, UP, 2>(s, sv, b, x, reset, done, st); break;
+        case 8: launch_rrs_t<8, BS, UP, 1>(s, sv, b, x, reset, done, st); break;
+        case 16: launch_rrs_t<16, BS, UP, 2>(s, sv, b, x, reset, done, st); break;
+        default: launch_rrs_t<32, BS, UP, 4>(s, sv, b, x, reset, done, st); break;
+    }
+}
+
 bool launch_bss(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
                 const int* done, cudaStream_t st, bool pad) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const double* sv = upper ? p.bss_up.p : p.bss_lo.p;
-    if (!pad || !s.bss || !sv || s.nitems == 0) return false;
+    if (!s.bss || !sv || s.nitems == 0) return false;
+    if (!an.bsr) {
+        if (pad) return false;
+        if (upper) {
+            if (an.bs == 3) launch_rrs_bs<3, true>(s, sv, b, x, reset, done, st);
+            else if (an.bs == 2) launch_rrs_bs<2, true>(s, sv, b, x, reset, done, st);
+            else launch_rrs_bs<1, true>(s, sv, b, x, reset, done, st);
+        } else {
+            if (an.bs == 3) launch_rrs_bs<3, false>(s, sv, b, x, reset, done, st);
+            else if (an.bs == 2) launch_rrs_bs<2, false>(s, sv, b, x, reset, done, st);
+            else launch_rrs_bs<1, false>(s, sv, b, x, reset, done, st);
+        }
+        return true;
+    }
+    if (!pad) return false;
     auto kern = upper ? bss_trsv_kernel<true> : bss_trsv_kernel<false>;
     static unsigned cap[2] = {0, 0};
     if (!cap[upper]) {

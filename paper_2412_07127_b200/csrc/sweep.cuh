@@ -938,6 +938,121 @@ rr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
     }
 }
 
+// Entry-lane sweep on the item-ordered stream (bss.cu, scalar / not node-
+// blocked matrices): rr_trsv_kernel with each slot's off-block entries
+// re-laid contiguously -- values, then the in-block entries and reciprocal
+// pivots -- and each entry's column with its block row in the low two bits
+// (code = col << 2 | t). The lane / entry mapping, FMA order, shuffle tree
+// and diagonal solve are rr_trsv_kernel's: bit-identical results.
+template <int LG, int BS, bool UPPER, int CH>
+__global__ void __launch_bounds__(RR_THREADS, RR_CTAS)
+rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __restrict__ scode,
+                const double* __restrict__ sval, const double* rhs, double* out, double* reset,
+                const int* __restrict__ done) {
+    if (done && *done) return;
+    constexpr int G = 32 / LG;
+    constexpr int NIB = BS * (BS - 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    int64_t it = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    auto hdr_at = [&](int64_t i) { return i < nitems ? __ldg(hdr + (i * G + grp)) : make_int4(-1, 0, 0, 0); };
+    int4 m = hdr_at(it), m1 = hdr_at(it + nwarps), m2 = hdr_at(it + 2 * nwarps), m3 = hdr_at(it + 3 * nwarps);
+    double rhs0[BS], rhs1[BS];
+#pragma unroll
+    for (int t = 0; t < BS; ++t) {
+        rhs0[t] = m.x >= 0 ? rhs[static_cast<int64_t>(m.x) * BS + t] : 0.0;
+        rhs1[t] = m1.x >= 0 ? rhs[static_cast<int64_t>(m1.x) * BS + t] : 0.0;
+    }
+    auto prefetch = [&](const int4& q) {
+        if (q.x >= 0) {
+            const uintptr_t v0 = reinterpret_cast<uintptr_t>(sval + static_cast<uint32_t>(q.z));
+            const uintptr_t v1 = v0 + 8 * static_cast<uintptr_t>(q.y + NIB + BS);
+            for (uintptr_t a = (v0 & ~uintptr_t(127)) + 128 * static_cast<uintptr_t>(gl); a < v1; a += 128 * LG)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+            if (gl == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(scode + static_cast<uint32_t>(q.w)));
+        }
+    };
+    prefetch(m);
+    prefetch(m1);
+    while (it < nitems) {
+        prefetch(m2);
+        const bool active = m.x >= 0;
+        const int64_t r0 = active ? static_cast<int64_t>(m.x) * BS : 0;
+        const int total = active ? m.y : 0;
+        const double* v = sval + static_cast<uint32_t>(m.z);
+        const int32_t* cd = scode + static_cast<uint32_t>(m.w);
+        double binv[BS], bin[NIB > 0 ? NIB : 1];
+        if (active && gl == 0) {
+#pragma unroll
+            for (int j = 0; j < NIB; ++j) bin[j] = __ldg(v + total + j);
+#pragma unroll
+            for (int t = 0; t < BS; ++t) binv[t] = __ldg(v + total + NIB + t);
+        }
+        double acc[BS];
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = 0.0;
+        const int tmax = __reduce_max_sync(0xffffffffu, total);
+        for (int base = 0; base < tmax; base += LG * CH) {
+            double vv[CH], xv[CH];
+            int32_t jj[CH];
+            int tt[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = base + c * LG + gl;
+                tt[c] = -1;
+                jj[c] = 0;
+                vv[c] = 0.0;
+                xv[c] = 0.0;
+                if (e < total) {
+                    const int32_t code = __ldg(cd + e);
+                    tt[c] = code & 3;
+                    jj[c] = code >> 2;
+                    vv[c] = __ldg(v + e);
+                    xv[c] = ld_relaxed(out + jj[c]);
+                }
+            }
+            bool pend = false;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
+            while (__any_sync(0xffffffffu, pend)) {
+                pend = false;
+#pragma unroll
+                for (int c = 0; c < CH; ++c)
+                    if (tt[c] >= 0 && is_pending(xv[c])) {
+                        xv[c] = ld_relaxed(out + jj[c]);
+                        pend |= is_pending(xv[c]);
+                    }
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int t = 0; t < BS; ++t)
+                    if (tt[c] == t) acc[t] = fma(vv[c], xv[c], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
+        if (active && gl == 0) {
+            double xb[BS];
+            solve_diag_block<BS, UPPER>(rhs0, acc, bin, binv, xb);
+#pragma unroll
+            for (int t = 0; t < BS; ++t) st_relaxed(out + r0 + t, xb[t]);
+        }
+        __syncwarp();
+        if (reset && active && gl < BS) reset[r0 + gl] = pending_value();
+        it += nwarps;
+        m = m1;
+        m1 = m2;
+        m2 = m3;
+        m3 = hdr_at(it + 3 * nwarps);
+#pragma unroll
+        for (int t = 0; t < BS; ++t) {
+            rhs0[t] = rhs1[t];
+            rhs1[t] = m1.x >= 0 ? rhs[static_cast<int64_t>(m1.x) * BS + t] : 0.0;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------
 // mbarrier / bulk-copy helpers (chain.cuh)
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
