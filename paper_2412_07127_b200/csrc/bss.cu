@@ -8,6 +8,13 @@
 
 namespace pclab_b200 {
 
+#ifdef BSS_TRACE  // developer trace (tools/bss_trace.py): not in the product build
+extern "C" int pclab_debug_bss_trace(void* p) {
+    unsigned long long* q = static_cast<unsigned long long*>(p);
+    return static_cast<int>(cudaMemcpyToSymbol(g_bss_trace, &q, sizeof(q)));
+}
+#endif
+
 namespace {
 
 inline unsigned gridn(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
@@ -41,9 +48,10 @@ __global__ void bss_headers(int64_t ns, const int32_t* __restrict__ slots, const
     for (int64_t n = lane; n < nb; n += 32) scol[coff[s] + n] = bcol[bp[b] + n] / 3;
 }
 
-// values of one slot (warp per slot): neighbour n's 3x3 block at 9n (row
-// t, column c at 3t + c), then the in-block entries in solve_diag_block's
-// order, then 1 / l_tt
+// values of one slot (warp per slot): entry (t, c) of neighbour n's 3x3
+// block at (3t + c) * nb + n -- entry-major, so the sweep's 16 lanes (one
+// neighbour each) read consecutive doubles with every load -- then the
+// in-block entries in solve_diag_block's order, then 1 / l_tt
 template <bool UPPER>
 __global__ void bss_values(int64_t ns, const int4* __restrict__ hdr, const int64_t* __restrict__ rp,
                            const double* __restrict__ vals, const double* __restrict__ invd,
@@ -58,7 +66,7 @@ __global__ void bss_values(int64_t ns, const int4* __restrict__ hdr, const int64
     double* v = sval + static_cast<uint32_t>(h.z);
     for (int idx = lane; idx < 9 * nb; idx += 32) {
         const int n = idx / 9, w = idx % 9, t = w / 3, c = w % 3;
-        v[idx] = vals[rp[3 * b + t] + (UPPER ? 3 - t : 0) + 3 * n + c];
+        v[w * nb + n] = vals[rp[3 * b + t] + (UPPER ? 3 - t : 0) + 3 * n + c];
     }
     if (lane == 0) {
         double* d = v + 9 * nb;

@@ -679,7 +679,8 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
 // Node-blocked sweep on the item-ordered stream (bss.cu): the 3x3 node-
 // blocked, padded PCG-loop case of bsr_trsv_kernel with the factor values
 // re-laid per slot of the schedule -- a slot's block holds its neighbour
-// blocks' 9 values contiguously (block-major, row-major inside a block),
+// blocks' values contiguously (entry-major: entry (t, c) of neighbour n at
+// (3t + c) * nb + n, so the 16 lanes of a block read consecutive doubles),
 // then the 3 strictly-lower / -upper in-block entries and the 3 reciprocal
 // pivots -- and the neighbour block ids beside them. A slot is one 16-byte
 // header {block, neighbours, value offset, column offset}; every address of
@@ -688,6 +689,14 @@ bsr_trsv_kernel(int64_t nitems, const int32_t* __restrict__ srec,
 // and diagonal solve as bsr_item: bit-identical results.
 #ifndef BSS_CTAS
 #define BSS_CTAS 7
+#endif
+#ifdef BSS_TRACE  // developer trace (tools/bss_trace.py): per node {item start, dependencies seen, published, last dependency}
+static __device__ unsigned long long* g_bss_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #endif
 template <bool UPPER>
 __global__ void __launch_bounds__(BSR_THREADS, BSS_CTAS)
@@ -719,6 +728,10 @@ bss_trsv_kernel(int nitems, const int4* __restrict__ hdr, const int32_t* __restr
         const bool active = h.x >= 0;
         const int64_t blk = active ? h.x : 0;
         const int nb = active ? h.y : 0;
+#ifdef BSS_TRACE
+        const unsigned long long tr0 = gtime();
+        int tr_cnt = 0, tr_dep = -1;
+#endif
         const double* v = sval + static_cast<uint32_t>(h.z);
         const int32_t* c = scol + static_cast<uint32_t>(h.w);
         double rc[BS] = {0.0, 0.0, 0.0}, bin[NIB], binv[BS];
@@ -747,11 +760,11 @@ bss_trsv_kernel(int nitems, const int4* __restrict__ hdr, const int32_t* __restr
             int32_t xb = 0;
             if (own) {
                 xb = __ldg(c + n);
-                const double* vn = v + 9 * n;
+                const double* vn = v + n;
 #pragma unroll
                 for (int t = 0; t < BS; ++t)
 #pragma unroll
-                    for (int cc = 0; cc < BS; ++cc) a[t][cc] = __ldg(vn + BS * t + cc);
+                    for (int cc = 0; cc < BS; ++cc) a[t][cc] = __ldg(vn + (BS * t + cc) * nb);
                 ld_relaxed_v4(out + 4 * static_cast<int64_t>(xb), xv);
             } else {
 #pragma unroll
@@ -764,19 +777,47 @@ bss_trsv_kernel(int nitems, const int4* __restrict__ hdr, const int32_t* __restr
                 if (pend) {
                     ld_relaxed_v4(out + 4 * static_cast<int64_t>(xb), xv);
                     pend = is_pending(xv[0]) || is_pending(xv[1]) || is_pending(xv[2]);
+#ifdef BSS_TRACE
+                    ++tr_cnt;
+#endif
                 }
             }
+#ifdef BSS_TRACE
+            {  // the lane that polled longest holds the last dependency
+                int mx = tr_cnt;
+#pragma unroll
+                for (int o = LG / 2; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const unsigned who = __ballot_sync(0xffffffffu, own && tr_cnt == mx && mx > 0) >> (grp * LG) & 0xffffu;
+                const int src = who ? grp * LG + __ffs(who) - 1 : lane;
+                const int dep = __shfl_sync(0xffffffffu, xb, src);
+                tr_dep = who ? dep : -1;
+                tr_cnt = mx;
+            }
+#endif
 #pragma unroll
             for (int t = 0; t < BS; ++t)
 #pragma unroll
                 for (int cc = 0; cc < BS; ++cc) acc[t] = fma(a[t][cc], xv[cc], acc[t]);
         }
+#ifdef BSS_TRACE
+        const unsigned long long tr1 = gtime();
+#endif
 #pragma unroll
         for (int t = 0; t < BS; ++t) acc[t] = group_sum<LG>(acc[t]);
         if (active && gl == 0) {
             double x[BS];
             solve_diag_block<BS, UPPER>(rc, acc, bin, binv, x);
             st_relaxed_v4(out + 4 * blk, x[0], x[1], x[2], 0.0);
+#ifdef BSS_TRACE
+            if (g_bss_trace) {
+                const unsigned long long tr2 = gtime();
+                g_bss_trace[4 * blk + 0] = tr0;
+                g_bss_trace[4 * blk + 1] = tr1;
+                g_bss_trace[4 * blk + 2] = tr2;
+                g_bss_trace[4 * blk + 3] = (static_cast<unsigned long long>(static_cast<unsigned>(tr_cnt)) << 32) |
+                                           static_cast<unsigned>(tr_dep);
+            }
+#endif
         }
         __syncwarp();
         if (reset && active && gl < BS) reset[4 * blk + gl] = pending_value();
@@ -1015,6 +1056,9 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
             bool pend = false;
 #pragma unroll
             for (int c = 0; c < CH; ++c) pend |= tt[c] >= 0 && is_pending(xv[c]);
+#ifdef RRS_PROBE_NODEP
+            pend = false;
+#endif
             while (__any_sync(0xffffffffu, pend)) {
                 pend = false;
 #pragma unroll

@@ -32,6 +32,10 @@ lo = dev_ms(lambda: pc.trsv_device(False, x.data_ptr(), y.data_ptr()))
 up = dev_ms(lambda: pc.trsv_device(True, x.data_ptr(), y.data_ptr()))
 bt = torch.from_numpy(b).cuda()
 xt = torch.zeros_like(bt)
-prof = pc.profile_device(bt.data_ptr(), xt.data_ptr(), 10)
+try:
+    prof = pc.profile_device(bt.data_ptr(), xt.data_ptr(), 10)
+    prof = {k: round(float(v), 4) for k, v in prof.items()}
+except P.PclabError as e:  # probe builds with wrong numerics
+    prof = repr(e)
 env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("PCLAB_"))
 print(f"[{env}] lower {lo:.3f} upper {up:.3f} profile {prof}", flush=True)
