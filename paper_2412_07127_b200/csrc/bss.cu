@@ -167,8 +167,50 @@ __global__ void rrs_values(int64_t ns, int bs, const int4* __restrict__ hdr, con
     }
 }
 
+__global__ void slot_max_entries(int64_t ns, const int4* __restrict__ hdr, int* __restrict__ mx) {
+    const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    int v = s < ns && hdr[s].x >= 0 ? hdr[s].y : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(mx, v);
+}
+
+// one 128-byte record per slot from the slot's header, codes and values
+// (16 doubles: 8 values, 8 int32 codes, in-block entry, 2 reciprocal pivots, block id)
+__global__ void rec_pack(int64_t ns, const int4* __restrict__ hdr, const int32_t* __restrict__ scode,
+                         const double* __restrict__ sval, double* __restrict__ rec) {
+    const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= 16 * ns) return;
+    const int64_t s = idx >> 4;
+    const int j = static_cast<int>(idx & 15);
+    const int4 h = hdr[s];
+    const int total = h.x >= 0 ? h.y : 0;
+    const double* v = sval + static_cast<uint32_t>(h.z);
+    const int32_t* cd = scode + static_cast<uint32_t>(h.w);
+    double o = 0.0;
+    if (j < 8) {
+        o = j < total ? v[j] : 0.0;
+    } else if (j < 12) {
+        const int c0 = 2 * (j - 8), c1 = c0 + 1;
+        const uint32_t a = static_cast<uint32_t>(c0 < total ? cd[c0] : -1);
+        const uint32_t b = static_cast<uint32_t>(c1 < total ? cd[c1] : -1);
+        o = __longlong_as_double(static_cast<long long>(a | (static_cast<uint64_t>(b) << 32)));
+    } else if (j < 15) {
+        o = h.x >= 0 ? v[total + (j - 12)] : 0.0;
+    } else {
+        o = __longlong_as_double(static_cast<long long>(h.x));
+    }
+    rec[idx] = o;
+}
+
+bool rec_enabled() {
+    static const bool on = !(getenv("PCLAB_REC") && atoi(getenv("PCLAB_REC")) == 0);
+    return on;
+}
+
 void build_one_scalar(Schedule& s, const DevCsr& M, int bs, bool upper, cudaStream_t st) {
     s.bss = false;
+    s.rec = false;
     const int64_t ns = s.nitems * s.per_item;
     if (ns == 0 || ns >= (1LL << 31) || bs > 3) return;
     DevBuf<int64_t> voff(ns + 1), coff(ns + 1);
@@ -185,6 +227,13 @@ void build_one_scalar(Schedule& s, const DevCsr& M, int bs, bool upper, cudaStre
     CK_LAUNCH();
     s.bss_nvals = nv;
     s.bss = true;
+    if (rec_enabled() && bs == 2 && s.lanes == 8 && s.per_item == 4) {
+        DevBuf<int> mx(1);
+        CK(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
+        slot_max_entries<<<gridn(ns, 256), 256, 0, st>>>(ns, s.bss_hdr.p, mx.p);
+        CK_LAUNCH();
+        s.rec = dev_read(mx.p, st) <= 8 && ns < (1LL << 30);
+    }
 }
 
 void build_one(Schedule& s, const BlockCols& bc, cudaStream_t st) {
@@ -226,6 +275,7 @@ void build_bss(Analysis& an, cudaStream_t st) {
         build_one_scalar(an.blk_up, an.upper, an.bs, true, st);
     }
     if (!(an.blk_lo.bss && an.blk_up.bss)) an.blk_lo.bss = an.blk_up.bss = false;
+    if (!(an.blk_lo.bss && an.blk_lo.rec && an.blk_up.rec)) an.blk_lo.rec = an.blk_up.rec = false;
 }
 
 void fill_bss(const Analysis& an, Precond& p, cudaStream_t st) {
@@ -243,6 +293,14 @@ void fill_bss(const Analysis& an, Precond& p, cudaStream_t st) {
                 rrs_values<false><<<gridn(ns * 32, 256), 256, 0, st>>>(ns, an.bs, s.bss_hdr.p, an.lower.rp.p,
                                                                       p.lvals.p, p.invd.p, out.p);
             CK_LAUNCH();
+            if (s.rec) {  // the sweeps read the records only
+                DevBuf<double>& rec = up ? p.rec_up : p.rec_lo;
+                rec.alloc(16 * ns);
+                rec_pack<<<gridn(16 * ns, 256), 256, 0, st>>>(ns, s.bss_hdr.p, s.bss_col.p, out.p, rec.p);
+                CK_LAUNCH();
+                CK(cudaStreamSynchronize(st));
+                out.reset();
+            }
             continue;
         }
         if (up)
@@ -288,6 +346,24 @@ bool launch_bss(const Analysis& an, const Precond& p, bool upper, const double* 
                 const int* done, cudaStream_t st, bool pad) {
     const Schedule& s = upper ? an.blk_up : an.blk_lo;
     const double* sv = upper ? p.bss_up.p : p.bss_lo.p;
+    if (!an.bsr && s.bss && s.rec && s.nitems > 0 && (upper ? p.rec_up.p : p.rec_lo.p)) {
+        if (pad) return false;
+        auto kern = upper ? rec_trsv_kernel<true> : rec_trsv_kernel<false>;
+        static unsigned cap[2] = {0, 0};
+        if (!cap[upper]) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RR_THREADS, 0));
+            if (const char* e = getenv("PCLAB_REC_CTAS")) per_sm = std::min(per_sm, std::max(atoi(e), 1));
+            cap[upper] = static_cast<unsigned>(std::max(per_sm, 1) * sm_count());
+        }
+        const double per_level = s.nlevels ? static_cast<double>(s.nitems) / s.nlevels : 1.0;
+        const int64_t warps = static_cast<int64_t>(6.0 * per_level) + 1;
+        const int64_t blocks = std::max<int64_t>((warps + RR_THREADS / 32 - 1) / (RR_THREADS / 32), sm_count());
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, cap[upper]));
+        kern<<<grid, RR_THREADS, 0, st>>>(s.nitems, upper ? p.rec_up.p : p.rec_lo.p, b, x, reset, done);
+        CK_LAUNCH();
+        return true;
+    }
     if (!s.bss || !sv || s.nitems == 0) return false;
     if (!an.bsr) {
         if (pad) return false;

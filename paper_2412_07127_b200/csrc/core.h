@@ -89,6 +89,8 @@ struct Schedule {
     int64_t bss_nvals = 0;
     DevBuf<int4> bss_hdr;     // [slots] {block, neighbours, value offset, column offset}
     DevBuf<int32_t> bss_col;  // neighbour block ids, slot after slot
+    // scalar blocks of 2 rows with <= 8 off-block entries: fixed 128-byte slot records (rec_trsv_kernel)
+    bool rec = false;
 };
 
 // Block-column view of a node-blocked CSR matrix (Analysis::bsr): block
@@ -171,6 +173,7 @@ struct Precond {
     DevBuf<double> invd;        // 1 / l_ii (both sweeps)
     DevBuf<unsigned char> stream_lo, stream_up;  // range-sweep streams (RangeSched)
     DevBuf<double> bss_lo, bss_up;               // item-ordered sweep values (bss.cu)
+    DevBuf<double> rec_lo, rec_up;               // 128-byte slot records (bss.cu, Schedule::rec)
     DevBuf<double> diag;        // Jacobi payload
     double sigma = 1.0;         // GNN edge scale
     int ic0_attempts = 0;

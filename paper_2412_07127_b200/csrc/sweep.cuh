@@ -1098,6 +1098,110 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
 }
 
 // ------------------------------------------------------------------------
+// Slot-record sweep (bss.cu: Schedule::rec) for scalar matrices whose blocks
+// of 2 rows have at most 8 off-block entries (5- / 7-point stencils): the
+// entry-lane sweep of rrs_trsv_kernel<8, 2> on ONE fixed 128-byte record per
+// slot -- 8 values, 8 entry codes (col << 2 | row in block, -1 unused), the
+// in-block entry, the two reciprocal pivots and the block id -- at
+// rec + 16 * (item * 4 + group). No header or offset stands between an item
+// and its data, so everything is requested before it is needed: the record
+// two items ahead, the right-hand side and the FIRST dependency poll one item
+// ahead (an item usually starts with its dependencies already in registers
+// and re-polls only the pending ones). Lane / entry mapping, FMA order,
+// shuffle tree and diagonal solve are rrs_trsv_kernel's: bit-identical.
+#ifndef REC_CTAS
+#define REC_CTAS 10
+#endif
+template <bool UPPER>
+__global__ void __launch_bounds__(RR_THREADS, REC_CTAS)
+rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rhs, double* out, double* reset,
+                const int* __restrict__ done) {
+    if (done && *done) return;
+    constexpr int LG = 8, G = 4, BS = 2;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / LG, gl = lane % LG;
+    // 32-bit item and slot indices (the launcher checks items * 4 < 2^31)
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5), nit = static_cast<int>(nitems);
+    int it = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    // a slot's record: value of lane gl at q[gl], its code at q[8] + 4 gl, diagonal data at q[12..15]
+    auto rec_of = [&](int i) { return rec + 16 * static_cast<int64_t>(i * G + grp); };
+    // Per-lane item state: the lane's entry (value, code) and ONE of the four
+    // diagonal doubles (lane 0 in-block entry, 1 and 2 the reciprocal pivots,
+    // 3 the block id) -- lane 0 collects them by shuffles once the
+    // dependencies are in (8 registers instead of 24 over the three stages in
+    // flight: 12 CTAs per SM, so a whole level of the 256^3 mesh is resident).
+    struct Item {
+        double val;
+        int32_t code;
+        double dg;
+    };
+    auto fetch = [&](int i) {
+        Item m;
+        m.val = 0.0;
+        m.code = -1;
+        m.dg = __longlong_as_double(-1LL);
+        if (i < nit) {
+            const double* q = rec_of(i);
+            m.val = __ldg(q + gl);
+            m.code = __ldg(reinterpret_cast<const int32_t*>(q + 8) + gl);
+            if (gl < 4) m.dg = __ldg(q + 12 + gl);
+        }
+        return m;
+    };
+    // stage 1 of an item (one item ahead): right-hand side (lane t holds row t's) and first poll
+    auto stage1 = [&](const Item& m, double& rh, double& xv) {
+        xv = 0.0;
+        rh = 0.0;
+        if (m.code >= 0) xv = ld_relaxed(out + (m.code >> 2));
+        const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, m.dg, 3, LG));
+        if (gl < BS && blk >= 0) rh = rhs[blk * BS + gl];
+    };
+    Item m0 = fetch(it), m1 = fetch(it + nw);
+    double rh0, rh1, xv0, xv1;
+    stage1(m0, rh0, xv0);
+    while (it < nit) {
+        const Item m2 = fetch(it + 2 * nw);
+        stage1(m1, rh1, xv1);
+        // ---- item: wait for the pending dependencies only
+        const bool has = m0.code >= 0;
+        const int col = has ? m0.code >> 2 : 0;
+        bool pend = has && is_pending(xv0);
+        while (__any_sync(0xffffffffu, pend)) {
+            if (pend) {
+                xv0 = ld_relaxed(out + col);
+                pend = is_pending(xv0);
+            }
+        }
+        const int t = m0.code & 3;
+        double acc[BS];
+        acc[0] = has && t == 0 ? fma(m0.val, xv0, 0.0) : 0.0;
+        acc[1] = has && t == 1 ? fma(m0.val, xv0, 0.0) : 0.0;
+        const double rhs1 = __shfl_sync(0xffffffffu, rh0, 1, LG);
+        const double binv0 = __shfl_sync(0xffffffffu, m0.dg, 1, LG);
+        const double binv1 = __shfl_sync(0xffffffffu, m0.dg, 2, LG);
+        const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, m0.dg, 3, LG));
+        acc[0] = group_sum<LG>(acc[0]);
+        acc[1] = group_sum<LG>(acc[1]);
+        if (gl == 0 && blk >= 0) {
+            const double rhv[BS] = {rh0, rhs1}, bin[1] = {m0.dg}, binv[BS] = {binv0, binv1};
+            double xb[BS];
+            solve_diag_block<BS, UPPER>(rhv, acc, bin, binv, xb);
+            // rows 2 blk and 2 blk + 1: one 16-byte publication (readers poll their own 8 bytes)
+            asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1,%2};" ::"l"(out + blk * BS), "d"(xb[0]), "d"(xb[1])
+                         : "memory");
+        }
+        __syncwarp();
+        if (reset && gl < BS && blk >= 0) reset[blk * BS + gl] = pending_value();
+        it += nw;
+        m0 = m1;
+        m1 = m2;
+        rh0 = rh1;
+        xv0 = xv1;
+    }
+}
+
+
+// ------------------------------------------------------------------------
 // mbarrier / bulk-copy helpers (chain.cuh)
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
