@@ -11,6 +11,7 @@
 // U->L slot map), which is exactly the reference's accumulation order
 // over the edge list; no atomics anywhere.
 #include "core.h"
+#include "gnn_math.cuh"
 
 namespace pclab_b200 {
 
@@ -51,7 +52,7 @@ __device__ __forceinline__ void mlp(const double* x, double* y) {
 #pragma unroll
         for (int h = 0; h < kH; ++h) hid[h] = fma(c_p[W1 + h * IN + i], x[i], hid[h]);
 #pragma unroll
-    for (int h = 0; h < kH; ++h) hid[h] = tanh(hid[h]);
+    for (int h = 0; h < kH; ++h) hid[h] = tanh_nb(hid[h]);
 #pragma unroll
     for (int o = 0; o < OUT; ++o) {
         double acc = c_p[B2 + o];
@@ -289,7 +290,7 @@ edge_kernel(int64_t ne, const int32_t* __restrict__ erow, const int32_t* __restr
                 double t = c_p[B1 + h + u];
                 if (!FIRST) t = fma(c_p[W1 + (h + u) * IN], pk, t);
                 t = fma(c_p[W1 + (h + u) * IN + (FIRST ? 0 : 1)], fk, t);
-                hid[h + u] = tanh(t + (u ? a.y : a.x) + (u ? b.y : b.x));
+                hid[h + u] = tanh_nb(t + (u ? a.y : a.x) + (u ? b.y : b.x));
             }
         }
         double y = c_p[B2];

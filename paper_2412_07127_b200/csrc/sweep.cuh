@@ -1112,6 +1112,9 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
 #ifndef REC_CTAS
 #define REC_CTAS 10
 #endif
+#ifndef REC_STAG
+#define REC_STAG 0  // ns between the two polls in flight (0: one poll)
+#endif
 template <bool UPPER>
 __global__ void __launch_bounds__(RR_THREADS, REC_CTAS)
 rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rhs, double* out, double* reset,
@@ -1166,12 +1169,43 @@ rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rh
         const bool has = m0.code >= 0;
         const int col = has ? m0.code >> 2 : 0;
         bool pend = has && is_pending(xv0);
+#if REC_STAG
+        // two polls in flight half a round trip apart: a publication is seen
+        // a quarter of a round trip after it lands, on average, instead of
+        // half. The stagger is set once per item, while the first re-poll is
+        // in flight anyway, and keeps itself: each poll is re-issued as it
+        // returns.
+        if (__any_sync(0xffffffffu, pend)) {
+            double xa = xv0, xc = xv0;
+            if (pend) xa = ld_relaxed(out + col);
+            __nanosleep(REC_STAG);
+            if (pend) xc = ld_relaxed(out + col);
+            while (true) {
+                if (pend && !is_pending(xa)) {
+                    xv0 = xa;
+                    pend = false;
+                }
+                if (!__any_sync(0xffffffffu, pend)) break;
+                if (pend) xa = ld_relaxed(out + col);
+                if (pend && !is_pending(xc)) {
+                    xv0 = xc;
+                    pend = false;
+                }
+                if (!__any_sync(0xffffffffu, pend)) break;
+                if (pend) xc = ld_relaxed(out + col);
+            }
+        }
+#else
         while (__any_sync(0xffffffffu, pend)) {
+#ifdef REC_BACKOFF
+            __nanosleep(REC_BACKOFF);
+#endif
             if (pend) {
                 xv0 = ld_relaxed(out + col);
                 pend = is_pending(xv0);
             }
         }
+#endif
         const int t = m0.code & 3;
         double acc[BS];
         acc[0] = has && t == 0 ? fma(m0.val, xv0, 0.0) : 0.0;

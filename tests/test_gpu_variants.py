@@ -117,3 +117,56 @@ def test_item_stream_sweep_bit_identical_to_csr_sweep():
         outs.append(out.stdout.strip())
     assert len(set(outs)) == 1, outs
 
+
+
+REC_BITS = r"""
+import hashlib, sys
+import numpy as np
+import torch
+sys.path.insert(0, {root!r})
+import paper_2412_07127_b200 as P
+h = hashlib.sha256()
+for m in (24, 33):
+    w = P.workloads.by_name("diffusion_fv_256").scaled(m)
+    a, b, model = P.workloads.build(w)
+    for kind in ("ic0", "gnnic"):
+        pc = P.Precond(a, kind, model if kind == "gnnic" else None)
+        r = torch.from_numpy(np.random.default_rng(2).standard_normal(a.n)).cuda()
+        y = torch.empty_like(r)
+        for upper in (False, True):
+            pc.trsv_device(upper, r.data_ptr(), y.data_ptr())
+            h.update(y.cpu().numpy().tobytes())
+        bt = torch.from_numpy(b).cuda()
+        xt = torch.zeros_like(bt)
+        rep = pc.solve_device(bt.data_ptr(), xt.data_ptr(), rel_tol=1e-8, max_iters=300)
+        h.update(xt.cpu().numpy().tobytes())
+        h.update(str(rep["iterations"]).encode())
+print(h.hexdigest())
+"""
+
+
+def test_record_sweep_bit_identical_to_item_stream_sweep():
+    """rec_trsv_kernel (one fixed 128-byte record per slot, everything
+    requested ahead; 7-point diffusion, blocks of 2 rows) against
+    rrs_trsv_kernel (PCLAB_REC=0): same lane / entry mapping, FMA order,
+    shuffle tree and diagonal solve -- sweeps and whole PCG solves are
+    bit-identical (even and odd mesh sizes: the odd one has idle slots)."""
+    outs = []
+    for env in ({"PCLAB_REC": "0"}, {}):
+        e = dict(os.environ, **env)
+        out = subprocess.run([sys.executable, "-c", REC_BITS.format(root=ROOT)], env=e, cwd=ROOT,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stdout + out.stderr
+        outs.append(out.stdout.strip())
+    assert len(set(outs)) == 1, outs
+
+
+def test_branch_free_tanh_matches_library():
+    """tanh_nb (csrc/gnn_math.cuh, the GNN kernels' tanh) against the CUDA
+    library's on 2^24 points of [-24, 24], 2^20 tiny arguments and the
+    special values: absolute difference below 1e-14 (tools/tanh_check.cu,
+    compiled by __graft_entry__.build())."""
+    exe = os.path.join(ROOT, "build", "tanh_check")
+    assert os.path.exists(exe), "build/tanh_check missing: run __graft_entry__.build()"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
