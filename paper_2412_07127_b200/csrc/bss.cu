@@ -192,8 +192,10 @@ __global__ void rec_pack(int64_t ns, const int4* __restrict__ hdr, const int32_t
         o = j < total ? v[j] : 0.0;
     } else if (j < 12) {
         const int c0 = 2 * (j - 8), c1 = c0 + 1;
-        const uint32_t a = static_cast<uint32_t>(c0 < total ? cd[c0] : -1);
-        const uint32_t b = static_cast<uint32_t>(c1 < total ? cd[c1] : -1);
+        // unused lanes repeat entry 0's column (a poll of the same sector) with the ignore bit
+        const int32_t idle = total > 0 ? (cd[0] & ~3) | 2 : 2;
+        const uint32_t a = static_cast<uint32_t>(c0 < total ? cd[c0] : idle);
+        const uint32_t b = static_cast<uint32_t>(c1 < total ? cd[c1] : idle);
         o = __longlong_as_double(static_cast<long long>(a | (static_cast<uint64_t>(b) << 32)));
     } else if (j < 15) {
         o = h.x >= 0 ? v[total + (j - 12)] : 0.0;

@@ -1101,7 +1101,7 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
 // Slot-record sweep (bss.cu: Schedule::rec) for scalar matrices whose blocks
 // of 2 rows have at most 8 off-block entries (5- / 7-point stencils): the
 // entry-lane sweep of rrs_trsv_kernel<8, 2> on ONE fixed 128-byte record per
-// slot -- 8 values, 8 entry codes (col << 2 | row in block, -1 unused), the
+// slot -- 8 values, 8 entry codes (col << 2 | row in block; unused lanes: entry 0's column with bit 1 set), the
 // in-block entry, the two reciprocal pivots and the block id -- at
 // rec + 16 * (item * 4 + group). No header or offset stands between an item
 // and its data, so everything is requested before it is needed: the record
@@ -1110,10 +1110,7 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
 // and re-polls only the pending ones). Lane / entry mapping, FMA order,
 // shuffle tree and diagonal solve are rrs_trsv_kernel's: bit-identical.
 #ifndef REC_CTAS
-#define REC_CTAS 10
-#endif
-#ifndef REC_STAG
-#define REC_STAG 0  // ns between the two polls in flight (0: one poll)
+#define REC_CTAS 9
 #endif
 template <bool UPPER>
 __global__ void __launch_bounds__(RR_THREADS, REC_CTAS)
@@ -1128,109 +1125,137 @@ rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rh
     int it = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     // a slot's record: value of lane gl at q[gl], its code at q[8] + 4 gl, diagonal data at q[12..15]
     auto rec_of = [&](int i) { return rec + 16 * static_cast<int64_t>(i * G + grp); };
-    // Per-lane item state: the lane's entry (value, code) and ONE of the four
+    // Per-lane item state: the lane's entry (value, code), ONE of the four
     // diagonal doubles (lane 0 in-block entry, 1 and 2 the reciprocal pivots,
-    // 3 the block id) -- lane 0 collects them by shuffles once the
-    // dependencies are in (8 registers instead of 24 over the three stages in
-    // flight: 12 CTAs per SM, so a whole level of the 256^3 mesh is resident).
+    // 3 the block id; lane 0 collects them by shuffles once the dependencies
+    // are in -- 2 registers instead of 8 per item in flight), the right-hand
+    // side (lane t holds row t's) and the first poll's result.
     struct Item {
         double val;
         int32_t code;
         double dg;
+        double rh;
+        double xv;
     };
-    auto fetch = [&](int i) {
-        Item m;
-        m.val = 0.0;
-        m.code = -1;
-        m.dg = __longlong_as_double(-1LL);
-        if (i < nit) {
+    // Every load below writes its destination register directly: a default
+    // value overwritten under a per-lane condition compiles to a load into a
+    // temporary and a predicated move that waits for the load on the spot
+    // (measured: a quarter of the sweep's time). Lanes without a use load a
+    // harmless duplicate instead.
+    auto fetch = [&](Item& m, int i) {
+        if (i < nit) {  // warp-uniform
             const double* q = rec_of(i);
             m.val = __ldg(q + gl);
             m.code = __ldg(reinterpret_cast<const int32_t*>(q + 8) + gl);
-            if (gl < 4) m.dg = __ldg(q + 12 + gl);
+            m.dg = __ldg(q + 12 + (gl & 3));
+        } else {
+            m.val = 0.0;
+            m.code = 2;
+            m.dg = __longlong_as_double(-1LL);
         }
-        return m;
+        // the item's four records (512 bytes) reach L2 four items ahead, so the
+        // loads above, two items ahead, are back within an item's time
+        if (i + 2 * nw < nit && lane < 4)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + 16 * static_cast<int64_t>((i + 2 * nw) * G + lane)));
     };
-    // stage 1 of an item (one item ahead): right-hand side (lane t holds row t's) and first poll
-    auto stage1 = [&](const Item& m, double& rh, double& xv) {
-        xv = 0.0;
-        rh = 0.0;
-        if (m.code >= 0) xv = ld_relaxed(out + (m.code >> 2));
+    // stage 1 of an item (one item ahead): right-hand side and first poll
+    auto stage1 = [&](Item& m) {
+        m.xv = ld_relaxed(out + (m.code >> 2));  // unused lanes repeat entry 0's column: same sector, ignored
         const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, m.dg, 3, LG));
-        if (gl < BS && blk >= 0) rh = rhs[blk * BS + gl];
+        m.rh = rhs[blk >= 0 ? blk * BS + (gl & 1) : 0];
     };
-    Item m0 = fetch(it), m1 = fetch(it + nw);
-    double rh0, rh1, xv0, xv1;
-    stage1(m0, rh0, xv0);
-    while (it < nit) {
-        const Item m2 = fetch(it + 2 * nw);
-        stage1(m1, rh1, xv1);
-        // ---- item: wait for the pending dependencies only
-        const bool has = m0.code >= 0;
-        const int col = has ? m0.code >> 2 : 0;
-        bool pend = has && is_pending(xv0);
-#if REC_STAG
-        // two polls in flight half a round trip apart: a publication is seen
-        // a quarter of a round trip after it lands, on average, instead of
-        // half. The stagger is set once per item, while the first re-poll is
-        // in flight anyway, and keeps itself: each poll is re-issued as it
-        // returns.
-        if (__any_sync(0xffffffffu, pend)) {
-            double xa = xv0, xc = xv0;
-            if (pend) xa = ld_relaxed(out + col);
-            __nanosleep(REC_STAG);
-            if (pend) xc = ld_relaxed(out + col);
-            while (true) {
-                if (pend && !is_pending(xa)) {
-                    xv0 = xa;
-                    pend = false;
-                }
-                if (!__any_sync(0xffffffffu, pend)) break;
-                if (pend) xa = ld_relaxed(out + col);
-                if (pend && !is_pending(xc)) {
-                    xv0 = xc;
-                    pend = false;
-                }
-                if (!__any_sync(0xffffffffu, pend)) break;
-                if (pend) xc = ld_relaxed(out + col);
-            }
-        }
-#else
+#ifdef BSS_TRACE
+    unsigned long long tr_prev = gtime();
+#endif
+    // one item: `a` is solved, `b` (the next) gets its stage 1, `c` is fetched
+    auto step = [&](Item& a, Item& b, Item& c) {
+        fetch(c, it + 2 * nw);
+#ifdef BSS_TRACE
+        const unsigned long long trf = gtime();
+#endif
+        stage1(b);
+        const bool has = (a.code & 2) == 0;
+        const int col = a.code >> 2;
+#ifdef BSS_TRACE
+        const unsigned long long tr0 = gtime();
+        int tr_cnt = 0;
+#endif
+        // wait for the pending dependencies only
+        double xv = a.xv;
+        bool pend = has && is_pending(xv);
         while (__any_sync(0xffffffffu, pend)) {
-#ifdef REC_BACKOFF
-            __nanosleep(REC_BACKOFF);
-#endif
             if (pend) {
-                xv0 = ld_relaxed(out + col);
-                pend = is_pending(xv0);
+                xv = ld_relaxed(out + col);
+                pend = is_pending(xv);
+#ifdef BSS_TRACE
+                ++tr_cnt;
+#endif
             }
         }
+#ifdef BSS_TRACE
+        int tr_dep = -1;
+        {
+            int mx = tr_cnt;
+#pragma unroll
+            for (int o = LG / 2; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const unsigned who = __ballot_sync(0xffffffffu, has && tr_cnt == mx && mx > 0) >> (grp * LG) & 0xffu;
+            const int src = who ? grp * LG + __ffs(who) - 1 : lane;
+            const int dep = __shfl_sync(0xffffffffu, col, src);
+            tr_dep = who ? dep / BS : -1;
+            tr_cnt = mx;
+        }
+        const unsigned long long tr1 = gtime();
 #endif
-        const int t = m0.code & 3;
+        const int t = a.code & 1;
         double acc[BS];
-        acc[0] = has && t == 0 ? fma(m0.val, xv0, 0.0) : 0.0;
-        acc[1] = has && t == 1 ? fma(m0.val, xv0, 0.0) : 0.0;
-        const double rhs1 = __shfl_sync(0xffffffffu, rh0, 1, LG);
-        const double binv0 = __shfl_sync(0xffffffffu, m0.dg, 1, LG);
-        const double binv1 = __shfl_sync(0xffffffffu, m0.dg, 2, LG);
-        const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, m0.dg, 3, LG));
+        acc[0] = has && t == 0 ? fma(a.val, xv, 0.0) : 0.0;
+        acc[1] = has && t == 1 ? fma(a.val, xv, 0.0) : 0.0;
+        const double rhs1 = __shfl_sync(0xffffffffu, a.rh, 1, LG);
+        const double binv0 = __shfl_sync(0xffffffffu, a.dg, 1, LG);
+        const double binv1 = __shfl_sync(0xffffffffu, a.dg, 2, LG);
+        const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, a.dg, 3, LG));
         acc[0] = group_sum<LG>(acc[0]);
         acc[1] = group_sum<LG>(acc[1]);
         if (gl == 0 && blk >= 0) {
-            const double rhv[BS] = {rh0, rhs1}, bin[1] = {m0.dg}, binv[BS] = {binv0, binv1};
+            const double rhv[BS] = {a.rh, rhs1}, bin[1] = {a.dg}, binv[BS] = {binv0, binv1};
             double xb[BS];
             solve_diag_block<BS, UPPER>(rhv, acc, bin, binv, xb);
             // rows 2 blk and 2 blk + 1: one 16-byte publication (readers poll their own 8 bytes)
             asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1,%2};" ::"l"(out + blk * BS), "d"(xb[0]), "d"(xb[1])
                          : "memory");
+#ifdef BSS_TRACE
+            if (g_bss_trace) {
+                g_bss_trace[4 * blk + 0] = tr0;
+                g_bss_trace[4 * blk + 1] = tr1;
+                g_bss_trace[4 * blk + 2] = gtime();
+                const unsigned long long gap = min(tr0 - tr_prev, 65535ULL);  // loop top: from the last item's end
+                const unsigned long long gapf = min(trf - tr_prev, 65535ULL);  // ... of which up to the fetch
+                g_bss_trace[4 * blk + 3] = (gap << 48) | (gapf << 32) | static_cast<unsigned>(tr_dep);
+                (void)tr_cnt;
+            }
+#endif
         }
+#ifdef BSS_TRACE
+        tr_prev = gtime();
+#endif
         __syncwarp();
         if (reset && gl < BS && blk >= 0) reset[blk * BS + gl] = pending_value();
         it += nw;
-        m0 = m1;
-        m1 = m2;
-        rh0 = rh1;
-        xv0 = xv1;
+    };
+    // the three items in flight trade roles instead of moving through
+    // registers: a move of a value still being loaded would stall the warp for
+    // the rest of the load's latency (measured: 0.8 us per item)
+    Item m0, m1, m2;
+    fetch(m0, it);
+    fetch(m1, it + nw);
+    stage1(m0);
+    while (true) {
+        if (it >= nit) break;
+        step(m0, m1, m2);
+        if (it >= nit) break;
+        step(m1, m2, m0);
+        if (it >= nit) break;
+        step(m2, m0, m1);
     }
 }
 

@@ -18,7 +18,8 @@ upper = len(sys.argv) > 2 and sys.argv[2] == "upper"
 w = P.workloads.by_name(name)
 a, b, model = P.workloads.build(w)
 pc = P.Precond(a, "ic0")
-nb = a.n // 3
+bsz = 3 if w.family == "elasticity" else 2
+nb = a.n // bsz
 x = torch.randn(a.n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 tr = torch.zeros(4 * nb, dtype=torch.int64, device="cuda")
@@ -32,7 +33,8 @@ torch.cuda.synchronize()
 L.pclab_debug_bss_trace(None)
 t = tr.cpu().numpy().reshape(nb, 4)
 t0, t1, t2 = t[:, 0].astype(np.int64), t[:, 1].astype(np.int64), t[:, 2].astype(np.int64)
-cnt = (t[:, 3].view(np.uint64) >> np.uint64(32)).astype(np.int64)
+cnt = ((t[:, 3].view(np.uint64) >> np.uint64(32)) & np.uint64(0xFFFF)).astype(np.int64)
+gap = (t[:, 3].view(np.uint64) >> np.uint64(48)).astype(np.int64)  # record sweep only: loop top of the item
 dep = (t[:, 3].view(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
 dep[dep == 0xFFFFFFFF] = -1
 base = t0[t0 > 0].min()
@@ -48,6 +50,12 @@ print("hop   ns (publish of the last dependency -> all seen):", q(hop))
 print("chain ns (all seen -> published):", q(chain))
 print("front ns (item start -> all seen, nodes that never re-polled):", q(front))
 print("wait  ns (item start -> all seen, nodes that re-polled):", q(t1[waited] - t0[waited]))
+if gap.max() > 0:
+    print("gap   ns (previous item's end -> item start, same warp):", q(gap))
+    print("  of which up to the issue of the record loads two items ahead (record sweep: field reused):", q(cnt))
+    late = t0[waited] - t2[dep[waited]]
+    print("late  ns (item start - publish of its last dependency; > 0: the warp arrived after it):", q(late),
+          "; late starts %.1f %%" % (100.0 * (late > 0).mean()))
 # critical path: back from the last publication
 cur = int(np.argmax(t2))
 hops = chains = late = 0
