@@ -74,12 +74,20 @@ def ncu_traffic(workload: str, kernel: str):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """nvidia-smi sampling during the timed region. The sampler is started
+    before the warm-up steps (its NVML attach can hold up a concurrent
+    cudaMalloc / cudaFree for ~0.2 s, which once landed in the first timed
+    preconditioner build) and mark() keeps only the samples taken after the
+    timed region began."""
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = 0
+
+    def mark(self):
+        self.first = len(self.lines)
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -110,7 +118,7 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.first:]:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 8:
                 continue
@@ -235,15 +243,16 @@ def run_b200(args, w):
         held.append(pc)
         return pc, rep
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     reps = []
-    l0 = P.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        l0 = P.launch_count()
+        clk.mark()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
@@ -267,9 +276,10 @@ def run_b200(args, w):
     lay = pc.layout()
     kern = T.iteration_kernels(pc, n, nnz, prof)
     if lay["node_blocked"]:
-        top, top_name = "sweep_lower", "bsr_trsv_kernel (node-blocked sweep)"
+        top, top_name = "sweep_lower", "bss_trsv_kernel (node-blocked sweep, item-ordered stream)"
     else:
-        top, top_name = "sweep_lower", "rr_trsv_kernel (lower sweep)"
+        top, top_name = "sweep_lower", ("rec_trsv_kernel (slot-record sweep)" if lay.get("slot_records")
+                                        else "rrs_trsv_kernel (entry-lane sweep)")
     csr_bytes = T.csr_iteration_bytes(nnz, info["nnz_lower"], n)
     iter_bytes = sum(k["bytes"] for k in kern.values())
     iter_ms = sum(k["ms"] for k in kern.values())

@@ -137,7 +137,8 @@ pclab_status pclab_precond_info(const pclab_precond* p, int64_t* nnz_lower,
 
 /* Device data layout of the sweeps and product (for traffic accounting):
  * out8 = [node-blocked sweeps, node-blocked A, block columns of L, of U,
- * of A, sweep slots lower, upper, lanes per block]. Zeros before analysis. */
+ * of A, sweep slots lower, upper, lanes per block (+ 1000 when the sweeps
+ * run on fixed 128-byte slot records)]. Zeros before analysis. */
 pclab_status pclab_precond_layout(const pclab_precond* p, int64_t* out8);
 /* Factor values in lower-triangle (row, col) order, as the reference's
  * LowerFactor stores them. Host or device destination. */

@@ -350,7 +350,7 @@ class Precond:
         _check(lib().pclab_precond_layout(self._h, t))
         return {"node_blocked": bool(t[0]), "a_node_blocked": bool(t[1]), "block_cols_lower": int(t[2]),
                 "block_cols_upper": int(t[3]), "block_cols_a": int(t[4]), "slots_lower": int(t[5]),
-                "slots_upper": int(t[6]), "lanes": int(t[7])}
+                "slots_upper": int(t[6]), "lanes": int(t[7]) % 1000, "slot_records": int(t[7]) >= 1000}
 
     def factor(self) -> np.ndarray:
         out = np.empty(max(self.info()["nnz_lower"], 1))

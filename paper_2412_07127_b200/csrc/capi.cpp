@@ -606,7 +606,7 @@ pclab_status pclab_precond_layout(const pclab_precond* p, int64_t* out8) {
     out8[4] = an->a_bsr ? an->abc.bcol.n : 0;
     out8[5] = an->blk_lo.nitems * an->blk_lo.per_item;
     out8[6] = an->blk_up.nitems * an->blk_up.per_item;
-    out8[7] = an->blk_lo.lanes;
+    out8[7] = an->blk_lo.lanes + (an->blk_lo.rec ? 1000 : 0);  // + 1000: fixed slot records (rec_trsv_kernel)
     return PCLAB_OK;
 }
 

@@ -53,9 +53,11 @@ print("wait  ns (item start -> all seen, nodes that re-polled):", q(t1[waited] -
 if gap.max() > 0:
     print("gap   ns (previous item's end -> item start, same warp):", q(gap))
     print("  of which up to the issue of the record loads two items ahead (record sweep: field reused):", q(cnt))
-    late = t0[waited] - t2[dep[waited]]
-    print("late  ns (item start - publish of its last dependency; > 0: the warp arrived after it):", q(late),
-          "; late starts %.1f %%" % (100.0 * (late > 0).mean()))
+late = t0[waited] - t2[dep[waited]]
+print("late  ns (item start - publish of its last dependency; > 0: the warp arrived after it):", q(late),
+      "; late starts %.1f %%" % (100.0 * (late > 0).mean()))
+ontime = late <= 0
+print("hop   ns, items whose warp was already waiting:", q(hop[ontime]))
 # critical path: back from the last publication
 cur = int(np.argmax(t2))
 hops = chains = late = 0
