@@ -699,9 +699,7 @@ Analysis& ensure_analysis(Matrix& m, cudaStream_t st) {
             }
         }
     }
-    // range-pipelined sweeps (range.cu) and the item-ordered value streams
-    // (bss.cu) on the final sweep layout
-    build_range_scheds(*an, st);
+    // the item-ordered value streams / slot records (bss.cu) on the final sweep layout
     build_bss(*an, st);
     // node-blocked A: the PCG product reads one column index per block
     an->a_bsr = false;

@@ -103,28 +103,6 @@ struct BlockCols {
     DevBuf<int32_t> bcol;  // [bp[nblocks]]
 };
 
-// Range-pipelined sweep schedule (range.cu). Nodes (blocks of bs rows) are
-// cut, in sweep order, into `nranges` contiguous ranges of `range_nodes`;
-// range r runs on CTA r % grid. Inside a range the nodes go in steps: one
-// (range, level) group, split so that a step's staged data fits a shared
-// memory stage. The per-factor stream (Precond::stream_lo / stream_up) holds
-// each step's data contiguously -- node headers, encoded neighbour columns,
-// values -- so a CTA moves one step with one bulk copy.
-struct RangeSched {
-    bool ok = false;
-    bool upper = false;
-    int bs = 1;
-    int64_t nb = 0;            // nodes
-    int64_t range_nodes = 0;   // R
-    int64_t nranges = 0, nsteps = 0;
-    int64_t stream_bytes = 0, max_step_bytes = 0;
-    DevBuf<int64_t> range_step;  // [nranges + 1] first step of each range
-    DevBuf<int4> steps;          // [nsteps] {stream offset / 16, bytes / 16, nodes, first position}
-    DevBuf<int32_t> order;       // [nb] node at each stream position
-    DevBuf<int32_t> step_of;     // [nb] step of each node
-    DevBuf<int32_t> nxt;         // [nb] first later step that reuses the node's ring slot
-};
-
 // Symbolic analysis of a structurally symmetric matrix (the reference's
 // lower_triangle + csr_transpose, sparse.cpp:137/189, done once on the
 // device): L pattern with A's lower values, U = L^T pattern, the slot map
@@ -142,7 +120,6 @@ struct Analysis {
     Schedule row_lo;         // bs = 1, one row per warp (IC(0))
     Schedule blk_lo, blk_up; // bs-blocked sweeps (triangular solves)
     Schedule rowlev_up;      // bs = 1 upper levels (reported only)
-    RangeSched rs_lo, rs_up; // range-pipelined sweeps (ok = built)
     double ms = 0.0;         // wall time of the analysis (CUDA events)
     uint64_t id = 0;         // unique per analysis (IC(0) mask cache key)
 };
@@ -171,7 +148,6 @@ struct Precond {
     DevBuf<double> lvals;       // factor values on L's pattern
     DevBuf<double> uvals;       // same values on U's pattern (gathered)
     DevBuf<double> invd;        // 1 / l_ii (both sweeps)
-    DevBuf<unsigned char> stream_lo, stream_up;  // range-sweep streams (RangeSched)
     DevBuf<double> bss_lo, bss_up;               // item-ordered sweep values (bss.cu)
     DevBuf<double> rec_lo, rec_up;               // 128-byte slot records (bss.cu, Schedule::rec)
     DevBuf<double> diag;        // Jacobi payload
@@ -251,13 +227,6 @@ void build_bss(Analysis& an, cudaStream_t st);
 void fill_bss(const Analysis& an, Precond& p, cudaStream_t st);
 bool launch_bss(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
                 const int* done, cudaStream_t st, bool pad);
-// range.cu: range-pipelined sweeps
-void build_range_scheds(Analysis& an, cudaStream_t st);
-void fill_range_streams(const Analysis& an, Precond& p, cudaStream_t st);
-bool launch_range_trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x,
-                       double* reset, const int* done, cudaStream_t st, bool pad);
-void range_trace_begin(const Analysis& an, bool upper, cudaStream_t st);  // PCLAB_RANGE_TRACE
-void range_trace_end(const Analysis& an, bool upper, cudaStream_t st);
 void launch_sweep(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
                   const int* done, unsigned* ctr, cudaStream_t st, bool pad);
 void reciprocal_diag(const Analysis& an, const double* lvals, double* invd, cudaStream_t st);

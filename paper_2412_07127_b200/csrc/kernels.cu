@@ -357,24 +357,15 @@ void launch_trsv(const Analysis& an, const double* vals, const double* invd, boo
     CK_LAUNCH();
 }
 
-// One sweep of a preconditioner: the range-pipelined kernel when its
-// schedule and stream exist (range.cu), else the round-robin / claim-based
-// sweeps above.
+// One sweep of a preconditioner: on the item-ordered streams / slot records
+// (bss.cu) when they exist, else the round-robin sweeps above on the L / U CSR.
 void launch_sweep(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, double* reset,
                   const int* done, unsigned* ctr, cudaStream_t st, bool pad) {
-    if (launch_range_trsv(an, p, upper, b, x, reset, done, st, pad)) return;
     if (launch_bss(an, p, upper, b, x, reset, done, st, pad)) return;
     launch_trsv(an, upper ? p.uvals.p : p.lvals.p, p.invd.p, upper, b, x, reset, done, ctr, st, pad);
 }
 
 void trsv(const Analysis& an, const Precond& p, bool upper, const double* b, double* x, cudaStream_t st) {
-    range_trace_begin(an, upper, st);
-    struct TraceEnd {
-        const Analysis& an;
-        bool upper;
-        cudaStream_t st;
-        ~TraceEnd() { range_trace_end(an, upper, st); }
-    } trace_end{an, upper, st};
     DevBuf<unsigned> ctr(1);
     CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
     fill_pending(x, an.lower.n, st);

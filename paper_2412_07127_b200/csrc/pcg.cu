@@ -574,7 +574,6 @@ std::unique_ptr<Precond> build_precond(Matrix& a, Kind kind, const Model* model,
     gather_upper(an, p->lvals.p, p->uvals.p, st);
     p->invd.alloc(n);
     reciprocal_diag(an, p->lvals.p, p->invd.p, st);
-    fill_range_streams(an, *p, st);
     fill_bss(an, *p, st);
     p->ms_total = total.ms();  // the analysis ran inside this interval
     return p;
