@@ -2,12 +2,14 @@
 
 Per launch, for the layout the kernels actually run on (Precond.layout()):
 
-* node-blocked sweep (bsr_trsv_kernel): every factor value once (8 B), one
-  column index per 3x3 block (4 B), one 16-byte slot record per slot, and
+* node-blocked sweep (bss_trsv_kernel): every factor value once (8 B), one
+  column index per 3x3 block (4 B), one 16-byte slot header per slot, and
   per row the right-hand side, 1/l_ii, the solution write and the re-arm
   write of the other sweep vector (4 x 8 B);
-* entry-lane sweep (rr_trsv_kernel, not node-blocked): value + column index
-  per entry (12 B), the slot records, the same 32 B per row;
+* entry-lane sweep (rec_trsv_kernel / rrs_trsv_kernel, not node-blocked):
+  value + column index per entry (12 B), 16 B per slot, the same 32 B per
+  row (the fixed 128-byte records of rec_trsv_kernel move 1.04x these bytes:
+  profiles/ncu_traffic.json);
 * product (k_pupdate + k_spmv_bsr_pap / k_spmv_pap): p <- z + beta p
   (24 B/row), A's values (8 B) + block or entry column indices, row / block
   pointers, p gathered once, q written;
