@@ -40,7 +40,8 @@ def sweep_bytes(lay: dict, nnz_lower: int, n: int, upper: bool, pad: bool = Fals
         # rhs (r plain / y padded), 1/l_ii, solution write, re-arm write
         per_row = (V4 if upper else 8) + 8 + V4 + 8 if pad else 32
         return int(8 * nnz_lower + 4 * bc + 16 * slots + per_row * n)
-    return 12 * nnz_lower + 16 * slots + 32 * n
+    # the backward sweep's re-arm of y is k_axpy's on the unpadded path
+    return 12 * nnz_lower + 16 * slots + (24 if upper else 32) * n
 
 
 def product_bytes(lay: dict, nnz: int, n: int, bs: int, pad: bool = False) -> int:
@@ -77,7 +78,9 @@ def iteration_kernels(pc, n: int, nnz: int, prof: dict) -> dict:
         "spmv_p": {"ms": prof["spmv_ms"], "bytes": prod},
     }
     v = V4 if pad else 8
-    kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": int((v + 40) * n)}  # p, q, x r/w, r r/w
+    # p, q, x r/w, r r/w (+ the re-arm of an unpadded y)
+    rearm = 8 if (info["nnz_lower"] > 0 and not pad) else 0
+    kern["axpy_norm"] = {"ms": prof["axpy_ms"], "bytes": int((v + 40 + rearm) * n)}
     kern["dot"] = {"ms": prof["dot_ms"], "bytes": int((8 + v) * n)}
     for k in kern.values():
         k["gbs"] = k["bytes"] / k["ms"] / 1e6 if k["ms"] > 0 else None
