@@ -1105,8 +1105,9 @@ rrs_trsv_kernel(int64_t nitems, const int4* __restrict__ hdr, const int32_t* __r
 // repeat entry 0's column with bit 1 set: a poll of the same sector, ignored),
 // the in-block entry, the two reciprocal pivots and the block id -- at
 // rec + 16 * (item * 4 + group). No header or offset stands between an item
-// and its data, so everything is requested before it is needed: the record
-// two items ahead, the right-hand side and the FIRST dependency poll one item
+// and its data, so everything is requested before it is needed: the entry
+// codes three items ahead, the values and the dependencies' sectors (an L2
+// prefetch) two, the right-hand side and the FIRST dependency poll one item
 // ahead (an item usually starts with its dependencies already in registers
 // and re-polls only the pending ones). Lane / entry mapping, FMA order,
 // shuffle tree and diagonal solve are rrs_trsv_kernel's: bit-identical.
@@ -1145,23 +1146,32 @@ rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rh
     // temporary and a predicated move that waits for the load on the spot
     // (measured: a quarter of the sweep's time). Lanes without a use load a
     // harmless duplicate instead.
-    auto fetch = [&](Item& m, int i) {
-        if (i < nit) {  // warp-uniform
-            const double* q = rec_of(i);
-            m.val = __ldg(q + gl);
-            m.code = __ldg(reinterpret_cast<const int32_t*>(q + 8) + gl);
-            m.dg = __ldg(q + 12 + (gl & 3));
-        } else {
-            m.val = 0.0;
+    // stage 3 of an item (three items ahead): its entry codes; its four
+    // records (512 bytes) reach L2 two items before that
+    auto stage3 = [&](Item& m, int i) {
+        if (i < nit)  // warp-uniform
+            m.code = __ldg(reinterpret_cast<const int32_t*>(rec_of(i) + 8) + gl);
+        else
             m.code = 2;
-            m.dg = __longlong_as_double(-1LL);
-        }
-        // the item's four records (512 bytes) reach L2 four items ahead, so the
-        // loads above, two items ahead, are back within an item's time
         if (i + 2 * nw < nit && lane < 4)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(rec + 16 * static_cast<int64_t>((i + 2 * nw) * G + lane)));
     };
-    // stage 1 of an item (one item ahead): right-hand side and first poll
+    // stage 2 (two items ahead): the dependencies' sectors are asked into L2
+    // -- a first poll of a value not yet published would otherwise wait for
+    // the pending marker to come back from DRAM (x does not fit in L2 beside
+    // the record stream) -- and the value and diagonal data are loaded
+    auto stage2 = [&](Item& m, int i) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(out + (m.code >> 2)));
+        if (i < nit) {
+            const double* q = rec_of(i);
+            m.val = __ldg(q + gl);
+            m.dg = __ldg(q + 12 + (gl & 3));
+        } else {
+            m.val = 0.0;
+            m.dg = __longlong_as_double(-1LL);
+        }
+    };
+    // stage 1 (one item ahead): right-hand side and first poll
     auto stage1 = [&](Item& m) {
         m.xv = ld_relaxed(out + (m.code >> 2));  // unused lanes repeat entry 0's column: same sector, ignored
         const long long blk = __double_as_longlong(__shfl_sync(0xffffffffu, m.dg, 3, LG));
@@ -1170,9 +1180,11 @@ rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rh
 #ifdef BSS_TRACE
     unsigned long long tr_prev = gtime();
 #endif
-    // one item: `a` is solved, `b` (the next) gets its stage 1, `c` is fetched
-    auto step = [&](Item& a, Item& b, Item& c) {
-        fetch(c, it + 2 * nw);
+    // one item: `a` is solved while `b`, `c` and `d` (the next three) go
+    // through stages 1, 2 and 3
+    auto step = [&](Item& a, Item& b, Item& c, Item& d) {
+        stage3(d, it + 3 * nw);
+        stage2(c, it + 2 * nw);
 #ifdef BSS_TRACE
         const unsigned long long trf = gtime();
 #endif
@@ -1245,20 +1257,25 @@ rec_trsv_kernel(int64_t nitems, const double* __restrict__ rec, const double* rh
         if (reset && gl < BS && blk >= 0) reset[blk * BS + gl] = pending_value();
         it += nw;
     };
-    // the three items in flight trade roles instead of moving through
+    // the four items in flight trade roles instead of moving through
     // registers: a move of a value still being loaded would stall the warp for
-    // the rest of the load's latency (measured: 0.8 us per item)
-    Item m0, m1, m2;
-    fetch(m0, it);
-    fetch(m1, it + nw);
+    // the rest of the load's latency
+    Item m0, m1, m2, m3;
+    stage3(m0, it);
+    stage3(m1, it + nw);
+    stage3(m2, it + 2 * nw);
+    stage2(m0, it);
+    stage2(m1, it + nw);
     stage1(m0);
     while (true) {
         if (it >= nit) break;
-        step(m0, m1, m2);
+        step(m0, m1, m2, m3);
         if (it >= nit) break;
-        step(m1, m2, m0);
+        step(m1, m2, m3, m0);
         if (it >= nit) break;
-        step(m2, m0, m1);
+        step(m2, m3, m0, m1);
+        if (it >= nit) break;
+        step(m3, m0, m1, m2);
     }
 }
 
