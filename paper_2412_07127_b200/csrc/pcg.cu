@@ -675,7 +675,7 @@ SolveReport pcg_solve(Matrix& a, const Precond& pc, const double* b, double* x, 
         if (factor) {
             CK(cudaMemsetAsync(S.p->ctr, 0, sizeof(unsigned) * 4, st));
             launch_sweep(*an, pc, false, r.p, y.p, z, nullptr, S.p->ctr, st, padz);
-            launch_sweep(*an, pc, true, y.p, z, y.p, nullptr, S.p->ctr + 1, st, padz);
+            launch_sweep(*an, pc, true, y.p, z, padz ? y.p : nullptr, nullptr, S.p->ctr + 1, st, padz);
         } else if (pc.kind == Kind::Jacobi) {
             k_jacobi<<<vgrid, kT, 0, st>>>(n, r.p, pc.diag.p, z, S.p);
         }
